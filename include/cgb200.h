@@ -1,0 +1,218 @@
+/*
+ * cgb200.h -- C ABI of the B200-native conegraph solver path.
+ *
+ * The reference (conegraph, Python) exposes this path as Python calls on
+ * operator / cone / solver objects.  Each entry point below replaces one
+ * of those calls; the reference file:line it stands in for is cited.
+ * Host code (paper_1609_03488_b200/*.py) binds this header with ctypes;
+ * INTEGRATION.md shows the binding a conegraph maintainer would add.
+ *
+ * Conventions
+ *   - All vectors are float64 DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors) unless a parameter says "host".
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - Every function returns 0 on success or a negative CGB_E* code; the
+ *     message of the last failure on the calling thread is available from
+ *     cgb_last_error().  There is no CPU fallback: without a usable
+ *     sm_100 device every compute call fails with CGB_ENODEV.
+ *   - A cgb_ctx owns the persistent-kernel resources (grid barrier,
+ *     reduction banks).  Calls sharing one ctx must be serialised on one
+ *     stream; use one ctx per stream for concurrency.
+ */
+#ifndef CGB200_H
+#define CGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGB_ABI_VERSION 1
+
+/* ---- error codes --------------------------------------------------------- */
+#define CGB_OK 0
+#define CGB_EINVAL (-1)   /* bad argument / inconsistent descriptor        */
+#define CGB_ENODEV (-2)   /* no usable CUDA device                          */
+#define CGB_ECUDA (-3)    /* CUDA runtime error (message has details)       */
+#define CGB_ENOMEM (-4)   /* device allocation failed                       */
+#define CGB_ECOOP (-5)    /* cooperative launch not possible                */
+
+/* ---- operator plans (linop.py) ------------------------------------------- */
+/* Leaf kinds: the primitive maps an operator expression lowers to.         */
+#define CGB_LEAF_IDENTITY 0 /* rows = cols = n                                */
+#define CGB_LEAF_DENSE 1    /* val row-major rows x cols, leading dim ld      */
+#define CGB_LEAF_CSR 2      /* rowptr[rows+1] (int64), colidx (int32), val     */
+#define CGB_LEAF_CONV1D 3   /* full conv, kernel val[k0]: rows n0+k0-1, cols n0 */
+#define CGB_LEAF_CORR1D 4   /* valid corr (adjoint of CONV1D): rows n0, cols n0+k0-1 */
+#define CGB_LEAF_CONV2D 5   /* full 2-d conv of n0 x n1 image, kernel k0 x k1 */
+#define CGB_LEAF_CORR2D 6   /* valid 2-d corr (adjoint of CONV2D)             */
+
+typedef struct cgb_leaf {
+  int32_t kind;
+  int32_t reserved;
+  int64_t rows, cols;
+  const double* val;      /* dense values / CSR values / conv kernel        */
+  const int64_t* rowptr;  /* CSR only                                       */
+  const int32_t* colidx;  /* CSR only                                       */
+  int64_t ld;             /* dense leading dimension                        */
+  int64_t k0, k1;         /* conv kernel extent(s)                          */
+  int64_t n0, n1;         /* conv signal / image extent(s)                  */
+} cgb_leaf;
+
+/* One block term: out[row_origin + i] += alpha * leaf(in[in_off + .])[i]   */
+typedef struct cgb_term {
+  int32_t leaf;        /* index into leaves                                  */
+  int32_t in_buf;      /* 0 = apply input, t+1 = plan temporary t            */
+  int64_t row_origin;  /* output row of leaf row 0                           */
+  int64_t in_off;      /* input index of leaf column 0                       */
+  double alpha;
+} cgb_term;
+
+/* A row range of one output buffer, all of whose rows see the same terms.  */
+typedef struct cgb_rowblock {
+  int64_t row_begin, row_end;
+  int32_t out_buf;     /* 0 = apply output, t+1 = plan temporary t           */
+  int32_t level;       /* execution level; 0 = last (writes final output)    */
+  int32_t term_begin, term_end; /* range into terms (empty => zero rows)     */
+} cgb_rowblock;
+
+/* Flattened lowering of one operator direction (forward or adjoint).        */
+typedef struct cgb_plan_desc {
+  int64_t in_len, out_len;
+  int32_t nleaves, nterms, nrowblocks, ntemps;
+  const cgb_leaf* leaves;         /* host arrays; copied by cgb_op_create    */
+  const cgb_term* terms;
+  const cgb_rowblock* rowblocks;  /* must tile every buffer it writes        */
+  const int64_t* temp_len;        /* ntemps entries                          */
+} cgb_plan_desc;
+
+typedef struct cgb_ctx cgb_ctx;
+typedef struct cgb_op cgb_op;
+typedef struct cgb_cones cgb_cones;
+
+/* Library / device */
+int cgb_abi_version(void);
+const char* cgb_last_error(void);
+/* Create the persistent-kernel context on `device`; fails with CGB_ENODEV
+ * unless the device is sm_100 (B200 class). */
+int cgb_ctx_create(int device, cgb_ctx** out);
+int cgb_ctx_destroy(cgb_ctx* ctx);
+/* grid geometry of the persistent kernels: {num_sms, blocks_per_sm, threads} */
+int cgb_ctx_geometry(const cgb_ctx* ctx, int32_t* out3);
+
+/* Operator = forward + adjoint plan.  Replaces linop.Operator
+ * (linop.py:266-321): adjoint derived structurally by the host lowering
+ * (linop.py:187-207) and shipped as its own plan. */
+int cgb_op_create(cgb_ctx* ctx, const cgb_plan_desc* fwd, const cgb_plan_desc* adj,
+                  cgb_op** out);
+int cgb_op_destroy(cgb_op* op);
+/* y = A x (adjoint=0) or y = A^T x (adjoint=1).
+ * Replaces Operator.forward / Operator.adjoint_apply (linop.py:299-307). */
+int cgb_op_apply(cgb_ctx* ctx, const cgb_op* op, int adjoint, const double* x, double* y,
+                 void* stream);
+
+/* ---- cones (cones.py) ------------------------------------------------------ */
+#define CGB_CONE_ZERO 0
+#define CGB_CONE_NONNEG 1
+#define CGB_CONE_SOC 2
+#define CGB_CONE_EXP 3
+int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, int32_t ncones,
+                     cgb_cones** out);
+int cgb_cones_destroy(cgb_cones* K);
+/* out = Pi_K(v) (dual=0) or Pi_{K*}(v) (dual=1); v, out length = total dim.
+ * Replaces cones.project_product / project_product_dual (cones.py:93-115)
+ * and the solver's in-graph dual projection (scs.py:250-283). */
+int cgb_cones_project(cgb_ctx* ctx, const cgb_cones* K, int dual, const double* v, double* out,
+                      void* stream);
+
+/* ---- conjugate gradient (cg.py) ------------------------------------------- */
+#define CGB_RECIPE_DIRECT 0  /* solve A x = b, A square SPD  (cg.py:64-68)     */
+#define CGB_RECIPE_NORMAL 1  /* solve (lam I + A^T A) x = b (cg.py:71-84)      */
+typedef struct cgb_cg_result {
+  int64_t iterations;
+  double final_residual_norm;  /* sqrt(r_norm_sq)                             */
+  double b_norm;
+  int32_t converged;           /* frn <= tol * ||b||  (cg.py:152-161)         */
+  int32_t reserved;
+} cgb_cg_result;
+/* x holds x_init on entry and the solution on exit.  Synchronises `stream`
+ * to fill *res (host).  Replaces cg.cg_solve (cg.py:164-165). */
+int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const double* b,
+                 double* x, double tol, int64_t max_iter, cgb_cg_result* res, void* stream);
+
+/* ---- homogeneous self-dual embedding solver (scs.py) ---------------------- */
+typedef struct cgb_scs_settings {       /* ScsSettings (scs.py:84-118)          */
+  double eps;
+  int64_t max_iters;
+  int64_t check_interval;
+  double cg_base_tol, cg_tol_cap, cg_tol_power, cg_eps_factor;
+  int64_t cg_max_iter;                  /* resolved (None -> 10 n)              */
+  double cert_tau_ratio;
+} cgb_scs_settings;
+
+typedef struct cgb_scs_problem {
+  int64_t n, m;
+  const cgb_op* A;
+  const cgb_cones* K;
+  const double* b;     /* m */
+  const double* c;     /* n */
+  const double* g;     /* n+m : cached (I+Q_z)^{-1} h from cgb_inner_solve   */
+  double denom;        /* 1 + h.g                                            */
+  double pr_scale;     /* 1 / (1 + ||b||)                                    */
+  double dr_scale;     /* 1 / (1 + ||c||)                                    */
+} cgb_scs_problem;
+
+/* Device buffers owned by the caller.  N = n + m + 1. */
+typedef struct cgb_scs_work {
+  double* u; double* v; double* w;   /* N each; w = u + v maintained          */
+  double* cgx;                        /* n : CG warm start (p1 of last iter)   */
+  double* tax;                        /* m : A cgx, tracked through CG updates */
+  double* gx;                         /* n : A^T A cgx, tracked likewise       */
+  double* r; double* p0; double* p1; double* q;  /* n each : CG vectors        */
+  double* t;                          /* m : A p scratch                       */
+  double* state;                      /* CGB_STATE_LEN doubles, see below      */
+} cgb_scs_work;
+
+/* state[] layout (all float64; integers stored exactly) */
+#define CGB_ST_K 0        /* iterations done                                  */
+#define CGB_ST_SINCE 1    /* iterations since last check                      */
+#define CGB_ST_STATUS 2   /* 0 running, 1 solved, 2 infeasible, 3 unbounded   */
+#define CGB_ST_CGT 3      /* total inner CG iterations                        */
+#define CGB_ST_PR 4       /* last computed primal residual                    */
+#define CGB_ST_DR 5       /* last computed dual residual                      */
+#define CGB_ST_GAP 6      /* last computed gap                                */
+#define CGB_ST_LASTCG 7   /* CG iterations of the last splitting iteration    */
+#define CGB_STATE_LEN 16
+
+/* Run splitting iterations on device until the status latches, k reaches
+ * settings->max_iters, or `max_steps` iterations have run in this call.
+ * All loop state lives in `work`, so calls resume where they stopped.
+ * resid_every_iter=1 evaluates the residual triple every iteration (trace
+ * mode); otherwise only on check iterations, which is all the status latch
+ * reads (scs.py:404-409).  Asynchronous on `stream`.
+ * Replaces the while-loop of build_scs_graph / solve_built
+ * (scs.py:314-469, 541-568). */
+int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_settings* st,
+                cgb_scs_work* work, int64_t max_steps, int resid_every_iter, void* stream);
+
+/* Inner block solve [[I, A^T], [-A, I]] z = (d1, d2) by CG on I + A^T A:
+ * rhs = d1 - A^T d2, z1 = CG(rhs, x0 = z1 on entry), z2 = d2 + A z1.
+ * z = (z1, z2) has length n + m; scratch needs 4n + 2m doubles.
+ * If hdot != NULL, *hdot = c.z1 + b.z2 (host) is also returned.
+ * Synchronises `stream`.  Replaces scs._solve_inner_block (scs.py:170-187),
+ * the engine of prepare_subspace / subspace_project (scs.py:190-214). */
+int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const double* d2,
+                    double* z, double tol, int64_t max_iter, const double* c, const double* b,
+                    double* scratch, cgb_cg_result* res, double* hdot, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+/* Run `iters` grid barriers (mode 0) or grid reductions (mode 1) in one
+ * persistent launch; time it with events on `stream` to get the per-phase
+ * synchronisation cost that bounds small problems. */
+int cgb_debug_barrier(cgb_ctx* ctx, int64_t iters, int mode, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGB200_H */

@@ -1,0 +1,344 @@
+"""Lowering of operator expressions to flat device plans.
+
+A plan is what one persistent kernel executes for y = A x: every leaf
+(dense / CSR / 1-d conv / 2-d conv / identity) becomes a *term*
+``out[row_origin + i] += alpha * leaf(in[in_off:])[i]``; the output rows
+are cut into *row blocks* that see a fixed term list, so each output
+element is produced by exactly one warp lane summing its terms -- no
+atomics, no zero-fill pass, deterministic.  Scale and VStack/HStack
+(adjoint-of-VStack) structure folds into alpha / offsets; Sum adds terms
+to the same rows; Compose of two non-trivial operators introduces a plan
+temporary produced one *level* earlier (a grid barrier apart).  The
+adjoint plan is lowered from the same tree with the adjoint flag pushed
+to the leaves (linop.py:187-207 rules), so Conv1D's adjoint is a valid
+correlation leaf, Dense's is the row-major transpose, CSC's is the CSR
+of the transpose.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from . import linop as L
+
+
+def _scaled_identity(e) -> float | None:
+    """alpha if e is alpha * Identity (through Scale/AdjointOf), else None."""
+    if isinstance(e, L.Identity):
+        return 1.0
+    if isinstance(e, L.Scale):
+        s = _scaled_identity(e.child)
+        return None if s is None else e.alpha * s
+    if isinstance(e, L.AdjointOf):
+        return _scaled_identity(e.child)
+    return None
+
+
+def _cuda(a: np.ndarray, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else a.astype(dtype)))
+    return t.to("cuda")
+
+
+def _leaf_buffers(e) -> dict:
+    """Device copies of a leaf's data, cached on the expression object."""
+    cache = getattr(e, "_cgb_dev", None)
+    if cache is None:
+        cache = {}
+        e._cgb_dev = cache
+    return cache
+
+
+class _Builder:
+    def __init__(self):
+        self.leaves: list[_lib.Leaf] = []
+        self.leaf_key: dict = {}
+        self.terms: list[tuple] = []  # (leaf, in_buf, row_origin, in_off, alpha, out_buf)
+        self.temp_len: list[int] = []
+        self.temp_level: list[int] = []
+        self.keep: list = []
+        self.algo_bytes = 0  # algorithmic bytes of one application (roofline)
+
+    # -- leaves -------------------------------------------------------------
+    def _add_leaf(self, key, make):
+        idx = self.leaf_key.get(key)
+        if idx is None:
+            leaf, nbytes = make()
+            idx = len(self.leaves)
+            self.leaves.append(leaf)
+            self.leaf_key[key] = idx
+        return idx
+
+    def leaf(self, e, adj: bool) -> int:
+        if isinstance(e, (L.DenseMatrix, L.SparseMatrix)) and e._transpose_of is not None:
+            e, adj = e._transpose_of, not adj
+        if isinstance(e, L.Identity):
+            n = e.rows
+            return self._add_leaf(("I", n), lambda: (_lib.Leaf(kind=_lib.LEAF_IDENTITY, rows=n,
+                                                               cols=n), 0))
+        if isinstance(e, L.DenseMatrix):
+            def make():
+                buf = _leaf_buffers(e)
+                key = "adj" if adj else "fwd"
+                if key not in buf:
+                    buf[key] = _cuda(e.values.T if adj else e.values)
+                t = buf[key]
+                self.keep.append(t)
+                rows, cols = (e.cols, e.rows) if adj else (e.rows, e.cols)
+                return _lib.Leaf(kind=_lib.LEAF_DENSE, rows=rows, cols=cols,
+                                 val=t.data_ptr(), ld=cols), 0
+            return self._add_leaf((id(e), adj), make)
+        if isinstance(e, L.SparseMatrix):
+            def make():
+                buf = _leaf_buffers(e)
+                key = "adj" if adj else "fwd"
+                if key not in buf:
+                    csc = e.matrix
+                    if adj:  # CSC of A == CSR of A^T
+                        ptr, idx, val = csc.indptr, csc.indices, csc.data
+                    else:
+                        csr = csc.tocsr()
+                        csr.sort_indices()
+                        ptr, idx, val = csr.indptr, csr.indices, csr.data
+                    buf[key] = (_cuda(ptr, np.int64), _cuda(idx, np.int32),
+                                _cuda(val, np.float64))
+                p, i, v = buf[key]
+                self.keep.extend((p, i, v))
+                rows, cols = (e.cols, e.rows) if adj else (e.rows, e.cols)
+                return _lib.Leaf(kind=_lib.LEAF_CSR, rows=rows, cols=cols, val=v.data_ptr(),
+                                 rowptr=p.data_ptr(), colidx=i.data_ptr()), 0
+            return self._add_leaf((id(e), adj), make)
+        if isinstance(e, L.Conv1D):
+            def make():
+                buf = _leaf_buffers(e)
+                if "kernel" not in buf:
+                    buf["kernel"] = _cuda(e.kernel)
+                t = buf["kernel"]
+                self.keep.append(t)
+                k, n = len(e.kernel), e.n
+                if adj:
+                    return _lib.Leaf(kind=_lib.LEAF_CORR1D, rows=n, cols=n + k - 1,
+                                     val=t.data_ptr(), k0=k, n0=n), 0
+                return _lib.Leaf(kind=_lib.LEAF_CONV1D, rows=n + k - 1, cols=n,
+                                 val=t.data_ptr(), k0=k, n0=n), 0
+            return self._add_leaf((id(e), adj), make)
+        if isinstance(e, L.Conv2D):
+            def make():
+                buf = _leaf_buffers(e)
+                if "kernel" not in buf:
+                    buf["kernel"] = _cuda(e.kernel)
+                t = buf["kernel"]
+                self.keep.append(t)
+                kh, kw = e.kernel.shape
+                h, w = e.image_shape
+                kind = _lib.LEAF_CORR2D if adj else _lib.LEAF_CONV2D
+                rows, cols = (e.cols, e.rows) if adj else (e.rows, e.cols)
+                return _lib.Leaf(kind=kind, rows=rows, cols=cols, val=t.data_ptr(), k0=kh,
+                                 k1=kw, n0=h, n1=w), 0
+            return self._add_leaf((id(e), adj), make)
+        raise L.LinOpError(f"no device leaf for {type(e).__name__}")
+
+    # -- lowering -------------------------------------------------------------
+    def new_temp(self, length: int, level: int) -> int:
+        self.temp_len.append(int(length))
+        self.temp_level.append(level)
+        return len(self.temp_len)  # buffer id (t+1)
+
+    def emit(self, e, adj, in_buf, in_off, out_buf, out_row, alpha, level):
+        if alpha == 0.0:
+            return
+        if isinstance(e, L.ZeroOp):
+            return
+        if isinstance(e, L.Scale):
+            self.emit(e.child, adj, in_buf, in_off, out_buf, out_row, alpha * e.alpha, level)
+            return
+        if isinstance(e, L.Sum):
+            self.emit(e.left, adj, in_buf, in_off, out_buf, out_row, alpha, level)
+            self.emit(e.right, adj, in_buf, in_off, out_buf, out_row, alpha, level)
+            return
+        if isinstance(e, L.AdjointOf):
+            self.emit(e.child, not adj, in_buf, in_off, out_buf, out_row, alpha, level)
+            return
+        if isinstance(e, L.VStack):
+            off = 0
+            for c in e.children:
+                if adj:   # sum_i child_i^T y[block i]
+                    self.emit(c, True, in_buf, in_off + off, out_buf, out_row, alpha, level)
+                else:     # stacked outputs
+                    self.emit(c, False, in_buf, in_off, out_buf, out_row + off, alpha, level)
+                off += c.rows
+            return
+        if isinstance(e, L.Compose):
+            first, second = (e.left, e.right) if adj else (e.right, e.left)
+            s1, s2 = _scaled_identity(first), _scaled_identity(second)
+            if s1 is not None:
+                self.emit(second, adj, in_buf, in_off, out_buf, out_row, alpha * s1, level)
+                return
+            if s2 is not None:
+                self.emit(first, adj, in_buf, in_off, out_buf, out_row, alpha * s2, level)
+                return
+            inner = e.right.rows
+            t = self.new_temp(inner, level + 1)
+            self.emit(first, adj, in_buf, in_off, t, 0, 1.0, level + 1)
+            self.emit(second, adj, t, 0, out_buf, out_row, alpha, level)
+            return
+        if isinstance(e, L.Kron):
+            raise NotImplementedError("Kron operators are not lowered to device plans yet")
+        rows = e.cols if adj else e.rows
+        if rows == 0 or (e.rows if adj else e.cols) == 0:
+            return
+        li = self.leaf(e, adj)
+        self.terms.append((li, in_buf, out_row, in_off, float(alpha), out_buf))
+
+    def finish(self, in_len: int, out_len: int):
+        buf_len = [out_len] + self.temp_len
+        # stage of a buffer = 1 + max stage of the buffers its terms read
+        # (input = stage 0); every term runs at its output buffer's stage.
+        writers: dict[int, list] = {b: [] for b in range(len(buf_len))}
+        for t in self.terms:
+            writers[t[5]].append(t)
+        stage: dict[int, int] = {}
+
+        def stage_of(buf: int) -> int:  # buffer id; -1 is the apply input
+            if buf == -1:
+                return 0
+            if buf not in stage:
+                srcs = [(-1 if t[1] == 0 else t[1]) for t in writers[buf]]
+                stage[buf] = 1 + max((stage_of(s) for s in srcs), default=0)
+            return stage[buf]
+
+        # temporaries that never reach the output (e.g. composed with a zero
+        # operator) are dropped: length 0, no terms
+        live = {0}
+        frontier = [0]
+        while frontier:
+            b = frontier.pop()
+            for t in writers[b]:
+                if t[1] != 0 and t[1] not in live:
+                    live.add(t[1])
+                    frontier.append(t[1])
+        for b in range(1, len(buf_len)):
+            if b not in live:
+                buf_len[b] = 0
+                writers[b] = []
+        self.terms = [t for t in self.terms if t[5] in live]
+        self.temp_len = buf_len[1:]
+        top = stage_of(0)
+        buf_level = [top - stage_of(b) if b in live else 1 for b in range(len(buf_len))]
+        if any(lv < 0 for lv in buf_level):
+            raise L.LinOpError("plan lowering produced an inconsistent stage order")
+        self.temp_level = buf_level[1:]
+        terms_c: list[_lib.Term] = []
+        rbs: list[_lib.RowBlock] = []
+        by_buf: dict[int, list] = {b: [] for b in range(len(buf_len))}
+        for t in self.terms:
+            by_buf[t[5]].append(t)
+        for b, length in enumerate(buf_len):
+            if length == 0:
+                continue
+            ts = by_buf[b]
+            cuts = {0, length}
+            for (li, _, r0, _, _, _) in ts:
+                cuts.add(r0)
+                cuts.add(r0 + self.leaves[li].rows)
+            cuts = sorted(c for c in cuts if 0 <= c <= length)
+            for a, z in zip(cuts[:-1], cuts[1:]):
+                if z <= a:
+                    continue
+                begin = len(terms_c)
+                for (li, ib, r0, io, al, _) in ts:
+                    if r0 <= a and z <= r0 + self.leaves[li].rows:
+                        terms_c.append(_lib.Term(leaf=li, in_buf=ib, row_origin=r0, in_off=io,
+                                                 alpha=al))
+                rbs.append(_lib.RowBlock(row_begin=a, row_end=z, out_buf=b, level=buf_level[b],
+                                         term_begin=begin, term_end=len(terms_c)))
+        arr_leaves = (_lib.Leaf * max(1, len(self.leaves)))(*self.leaves)
+        arr_terms = (_lib.Term * max(1, len(terms_c)))(*terms_c)
+        arr_rbs = (_lib.RowBlock * max(1, len(rbs)))(*rbs)
+        arr_tl = (ctypes.c_int64 * max(1, len(self.temp_len)))(*self.temp_len)
+        desc = _lib.PlanDesc(in_len=in_len, out_len=out_len, nleaves=len(self.leaves),
+                             nterms=len(terms_c), nrowblocks=len(rbs),
+                             ntemps=len(self.temp_len), leaves=arr_leaves, terms=arr_terms,
+                             rowblocks=arr_rbs, temp_len=arr_tl)
+        self.keep_c = (arr_leaves, arr_terms, arr_rbs, arr_tl)
+        self.nlevels = 1 + max(self.temp_level, default=0)
+        self.nrowblocks = len(rbs)
+        self.nterms = len(terms_c)
+        return desc
+
+
+def _leaf_algo_bytes(leaf: _lib.Leaf) -> int:
+    """Compulsory HBM bytes of one leaf application (read operands once)."""
+    k = leaf.kind
+    if k == _lib.LEAF_IDENTITY:
+        return 8 * leaf.rows
+    if k == _lib.LEAF_DENSE:
+        return 8 * leaf.rows * leaf.cols + 8 * leaf.cols
+    if k == _lib.LEAF_CSR:
+        return 0  # filled by caller from nnz
+    if k in (_lib.LEAF_CONV1D, _lib.LEAF_CORR1D, _lib.LEAF_CONV2D, _lib.LEAF_CORR2D):
+        return 8 * leaf.cols
+    return 0
+
+
+class DeviceOp:
+    """Compiled forward + adjoint plans of one expression (a cgb_op)."""
+
+    def __init__(self, expr):
+        self.ctx = _lib.device_context()
+        self.rows, self.cols = expr.rows, expr.cols
+        self.fwd = _Builder()
+        self.fwd.emit(expr, False, 0, 0, 0, 0, 1.0, 0)
+        self.adj = _Builder()
+        self.adj.emit(expr, True, 0, 0, 0, 0, 1.0, 0)
+        self.handle = None
+        self._empty = self.rows == 0 or self.cols == 0
+        if self._empty:
+            return
+        fdesc = self.fwd.finish(self.cols, self.rows)
+        adesc = self.adj.finish(self.rows, self.cols)
+        h = ctypes.c_void_p()
+        lib = _lib.load_library()
+        _lib.check(lib.cgb_op_create(self.ctx.handle, ctypes.byref(fdesc), ctypes.byref(adesc),
+                                     ctypes.byref(h)))
+        self.handle = h
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.cgb_op_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+
+    def apply(self, x, out=None, adjoint: bool = False):
+        import torch
+        n_out = self.cols if adjoint else self.rows
+        if out is None:
+            out = torch.empty(n_out, dtype=torch.float64, device=x.device)
+        if self._empty:
+            out.zero_()
+            return out
+        _lib.check(self._lib.cgb_op_apply(self.ctx.handle, self.handle, int(adjoint),
+                                          _lib.ptr(x), _lib.ptr(out), _lib.stream_handle()))
+        return out
+
+    def plan_info(self, adjoint: bool = False) -> dict:
+        b = self.adj if adjoint else self.fwd
+        return {"leaves": len(b.leaves), "terms": getattr(b, "nterms", 0),
+                "rowblocks": getattr(b, "nrowblocks", 0), "levels": getattr(b, "nlevels", 1),
+                "temps": len(b.temp_len)}
+
+    def algo_bytes(self, adjoint: bool = False) -> int:
+        """Compulsory bytes of one application: operand reads + output write."""
+        b = self.adj if adjoint else self.fwd
+        total = 0
+        for t in b.terms:
+            leaf = b.leaves[t[0]]
+            total += _leaf_algo_bytes(leaf)
+        n_out = self.cols if adjoint else self.rows
+        return total + 8 * n_out + 8 * sum(b.temp_len) * 2

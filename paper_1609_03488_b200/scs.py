@@ -1,0 +1,411 @@
+"""Homogeneous self-dual embedding splitting solver on the B200.
+
+Mirrors conegraph.scs (scs.py:1-576): ConeProblem, ScsSettings,
+ScsIterate, ScsSolution, prepare_subspace, subspace_project, residuals,
+build_scs_graph, iterate_states, solve_built, solve -- same arithmetic,
+same statuses, same iteration semantics (status latched every
+``check_interval`` iterations, CG warm-started from the previous p1 with
+the graph's tolerance schedule).
+
+Execution: ``build_scs_graph`` compiles the operator plans and cones and
+runs the one-time setup solve g = (I+Q_z)^{-1} h on device; the splitting
+loop then runs inside ONE persistent cooperative kernel (``cgb_scs_run``)
+that keeps every iterate in HBM and takes all loop decisions on device:
+the host does not synchronise per iteration, or per CG step, at all.
+Final classification (scs.py:497-538) reads u, v back once and evaluates
+the residuals with device operator applications.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import warnings
+from dataclasses import dataclass
+from typing import Iterator
+
+import numpy as np
+
+from . import _lib
+from .cones import ConeProduct
+from .linop import Operator
+
+SOLVED = "solved"
+INACCURATE = "inaccurate"
+MAX_ITERS = "max-iters"
+INFEASIBLE = "infeasible"
+UNBOUNDED = "unbounded"
+
+_STATUS_RUNNING = 0.0
+_STATUS_SOLVED = 1.0
+_STATUS_INFEASIBLE = 2.0
+_STATUS_UNBOUNDED = 3.0
+
+SMALL_TAU = 1e-12
+
+# loop-variable order of iterate_states (matches the reference graph)
+_IU, _IV, _IK, _ISINCE, _ISTATUS, _ICGW, _ICGT, _IRESID = range(8)
+
+
+@dataclass
+class ConeProblem:
+    """Cone program data in the equality convention A x + s = b, s in K."""
+
+    A: Operator
+    b: np.ndarray
+    c: np.ndarray
+    K: ConeProduct
+
+    def __post_init__(self) -> None:
+        self.b = np.asarray(self.b, dtype=np.float64)
+        self.c = np.asarray(self.c, dtype=np.float64)
+        m, n = self.A.shape
+        if self.b.shape != (m,):
+            raise ValueError(f"b has shape {self.b.shape}, expected ({m},)")
+        if self.c.shape != (n,):
+            raise ValueError(f"c has shape {self.c.shape}, expected ({n},)")
+        if self.K.total_dim != m:
+            raise ValueError(f"cone product has dim {self.K.total_dim}, expected {m}")
+
+    @property
+    def dims(self) -> tuple[int, int]:
+        return (self.A.cols, self.A.rows)
+
+
+@dataclass
+class ScsSettings:
+    """Solver knobs (scs.py:84-118), same fields, defaults and validation."""
+
+    eps: float = 1e-3
+    max_iters: int = 5000
+    check_interval: int = 20
+    cg_base_tol: float = 1e-9
+    cg_tol_cap: float = 0.1
+    cg_tol_power: float = 1.25
+    cg_eps_factor: float = 0.1
+    cg_max_iter: int | None = None
+    setup_cg_tol: float = 1e-12
+    cert_tau_ratio: float = 1e-6
+
+    def __post_init__(self) -> None:
+        if self.eps <= 0:
+            raise ValueError("eps must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.cg_tol_power not in (0.5, 1.0, 1.25, 1.5, 2.0):
+            raise ValueError("cg_tol_power must be one of 0.5, 1.0, 1.25, 1.5, 2.0")
+
+    def cg_tolerance(self, k: int) -> float:
+        raw = max(1.0 / (k + 1) ** self.cg_tol_power, self.cg_eps_factor * self.eps)
+        return max(self.cg_base_tol, min(self.cg_tol_cap, raw))
+
+    def to_c(self, n: int) -> _lib.ScsSettingsC:
+        cg_max = self.cg_max_iter if self.cg_max_iter is not None else 10 * n
+        return _lib.ScsSettingsC(
+            eps=self.eps, max_iters=int(self.max_iters), check_interval=int(self.check_interval),
+            cg_base_tol=self.cg_base_tol, cg_tol_cap=self.cg_tol_cap,
+            cg_tol_power=self.cg_tol_power, cg_eps_factor=self.cg_eps_factor,
+            cg_max_iter=int(cg_max), cert_tau_ratio=self.cert_tau_ratio)
+
+
+@dataclass
+class ScsIterate:
+    """Embedding iterates u = (x, y, tau), v = (0, s, kappa)."""
+
+    u: np.ndarray
+    v: np.ndarray
+
+
+@dataclass
+class ScsSolution:
+    status: str
+    x: np.ndarray
+    y: np.ndarray
+    s: np.ndarray
+    pobj: float
+    dobj: float
+    primal_residual: float
+    dual_residual: float
+    gap: float
+    iterations: int
+    avg_cg_iterations: float
+
+
+@dataclass
+class TraceRecord:
+    iteration: int
+    primal: float
+    dual: float
+    gap: float
+    cg_iters: int
+    u: np.ndarray
+    v: np.ndarray
+
+
+def _own_device_op(op: Operator):
+    """A DeviceOp whose forward plan is ``op``'s forward (never flipped)."""
+    dev, flip = op.device_op()
+    if flip:
+        from ._plan import DeviceOp
+        dev = DeviceOp(op.expr)
+    return dev
+
+
+def _cuda(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to("cuda")
+
+
+# -- subspace projection (scs.py:155-214) -------------------------------------
+
+@dataclass
+class PrecomputedSolve:
+    """Cached pieces of the (I+Q) solve: h = (c, b), g = (I+Q_z)^{-1} h."""
+
+    A: Operator
+    h: np.ndarray
+    g: np.ndarray
+    denom: float
+    cg_tol: float
+    cg_max_iter: int | None
+    setup_cg_iters: int = 0
+    g_device: object = None
+    c_device: object = None
+    b_device: object = None
+
+
+def _inner_solve(dev, d1, d2, tol, max_iter, c_dev=None, b_dev=None):
+    """Device [[I, A^T], [-A, I]] z = (d1, d2) (scs.py:170-187)."""
+    import torch
+    n, m = dev.cols, dev.rows
+    z = torch.zeros(n + m, dtype=torch.float64, device="cuda")
+    scratch = torch.empty(4 * n + 2 * m + 1, dtype=torch.float64, device="cuda")
+    res = _lib.CgResult()
+    hdot = ctypes.c_double(0.0)
+    if max_iter is None:
+        max_iter = 10 * n
+    _lib.check(_lib.load_library().cgb_inner_solve(
+        dev.ctx.handle, dev.handle, _lib.ptr(d1), _lib.ptr(d2), _lib.ptr(z), float(tol),
+        int(max_iter), _lib.ptr(c_dev), _lib.ptr(b_dev), _lib.ptr(scratch), ctypes.byref(res),
+        ctypes.byref(hdot), _lib.stream_handle()))
+    if not res.converged:
+        warnings.warn(
+            f"inner CG stopped at residual {res.final_residual_norm:.3e} after "
+            f"{res.iterations} iterations without reaching tolerance {tol:g}; the subspace "
+            f"step is inaccurate", RuntimeWarning, stacklevel=3)
+    return z, res, hdot.value
+
+
+def prepare_subspace(problem: ConeProblem, cg_tol: float = 1e-12,
+                     cg_max_iter: int | None = None) -> PrecomputedSolve:
+    """One-time high-accuracy solve used by every later subspace step (scs.py:190-196)."""
+    dev = _own_device_op(problem.A)
+    c_d, b_d = _cuda(problem.c), _cuda(problem.b)
+    z, res, hdot = _inner_solve(dev, c_d, b_d, cg_tol, cg_max_iter, c_d, b_d)
+    h = np.concatenate([problem.c, problem.b])
+    g = z.cpu().numpy()
+    denom = 1.0 + hdot
+    return PrecomputedSolve(problem.A, h, g, denom, cg_tol, cg_max_iter, int(res.iterations),
+                            z, c_d, b_d)
+
+
+def subspace_project(w, cached: PrecomputedSolve) -> np.ndarray:
+    """Solve (I + Q) out = w with the cached rank-one reduction (scs.py:199-214)."""
+    A = cached.A
+    n, m = A.cols, A.rows
+    w = np.asarray(w, dtype=np.float64)
+    if w.shape != (n + m + 1,):
+        raise ValueError(f"w has shape {w.shape}, expected ({n + m + 1},)")
+    dev = _own_device_op(A)
+    wd = _cuda(w)
+    c_d = cached.c_device if cached.c_device is not None else _cuda(cached.h[:n])
+    b_d = cached.b_device if cached.b_device is not None else _cuda(cached.h[n:])
+    p, _, hdot = _inner_solve(dev, wd[:n], wd[n:n + m], cached.cg_tol, cached.cg_max_iter,
+                              c_d, b_d)
+    tau = (w[-1] + hdot) / cached.denom
+    z = p.cpu().numpy() - tau * cached.g
+    return np.concatenate([z, [tau]])
+
+
+def residuals(iterate: ScsIterate, problem: ConeProblem) -> tuple[float, float, float]:
+    """Relative primal/dual residuals and gap (scs.py:217-244), device applies."""
+    A, b, c = problem.A, problem.b, problem.c
+    n, m = A.cols, A.rows
+    u, v = np.asarray(iterate.u), np.asarray(iterate.v)
+    ux, uy, tau = u[:n], u[n:n + m], u[-1]
+    vs = v[n:n + m]
+    if tau > SMALL_TAU:
+        x, y, s = ux / tau, uy / tau, vs / tau
+        pr = np.linalg.norm(A.forward(x) + s - b) / (1.0 + np.linalg.norm(b))
+        dr = np.linalg.norm(A.adjoint_apply(y) + c) / (1.0 + np.linalg.norm(c))
+        ct, bt = float(c @ x), float(b @ y)
+        gap = abs(ct + bt) / (1.0 + abs(ct) + abs(bt))
+        return float(pr), float(dr), float(gap)
+    den_u = -float(c @ ux)
+    den_i = -float(b @ uy)
+    pr = np.linalg.norm(A.forward(ux) + vs) / den_u if den_u > 0 else np.inf
+    dr = np.linalg.norm(A.adjoint_apply(uy)) / den_i if den_i > 0 else np.inf
+    return float(pr), float(dr), np.inf
+
+
+# -- the compiled solver ("graph") ---------------------------------------------------
+
+class SolverPlan:
+    """What build_scs_graph returns: compiled plans, cones, setup solve and
+    the device work buffers of the persistent splitting kernel."""
+
+    def __init__(self, problem: ConeProblem, settings: ScsSettings):
+        import torch
+        self.problem = problem
+        self.settings = settings
+        self.n, self.m = problem.A.cols, problem.A.rows
+        self.dev = _own_device_op(problem.A)
+        self.cones = problem.K.device()
+        self.cached = prepare_subspace(problem, settings.setup_cg_tol, settings.cg_max_iter)
+        n, m = self.n, self.m
+        N = n + m + 1
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.buf = {nm: torch.zeros(N, **f64) for nm in ("u", "v", "w")}
+        for nm in ("cgx", "gx", "r", "p0", "p1", "q"):
+            self.buf[nm] = torch.zeros(n, **f64)
+        for nm in ("tax", "t"):
+            self.buf[nm] = torch.zeros(m, **f64)
+        self.buf["state"] = torch.zeros(_lib.STATE_LEN, **f64)
+        self.work = _lib.ScsWorkC(**{nm: t.data_ptr() for nm, t in self.buf.items()})
+        ca = self.cached
+        self.cprob = _lib.ScsProblemC(
+            n=n, m=m, A=self.dev.handle.value, K=self.cones.handle.value,
+            b=ca.b_device.data_ptr(), c=ca.c_device.data_ptr(), g=ca.g_device.data_ptr(),
+            denom=ca.denom, pr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.b))),
+            dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))))
+        self.csettings = settings.to_c(n)
+        self.reset()
+
+    def reset(self) -> None:
+        """u = v = (0, 0, 1), w = u + v, warm start 0 (scs.py:448-458)."""
+        for t in self.buf.values():
+            t.zero_()
+        self.buf["u"][-1] = 1.0
+        self.buf["v"][-1] = 1.0
+        self.buf["w"][-1] = 2.0
+
+    def run(self, max_steps: int, resid_every_iter: bool = False) -> None:
+        """Asynchronous: enqueue up to max_steps splitting iterations."""
+        _lib.check(_lib.load_library().cgb_scs_run(
+            self.dev.ctx.handle, ctypes.byref(self.cprob), ctypes.byref(self.csettings),
+            ctypes.byref(self.work), int(max_steps), int(bool(resid_every_iter)),
+            _lib.stream_handle()))
+
+    def state(self) -> np.ndarray:
+        return self.buf["state"].cpu().numpy()
+
+    def loop_vars(self) -> list:
+        st = self.state()
+        return [self.buf["u"].cpu().numpy(), self.buf["v"].cpu().numpy(),
+                np.array([st[_lib.ST_K]]), np.array([st[_lib.ST_SINCE]]),
+                np.array([st[_lib.ST_STATUS]]), self.buf["cgx"].cpu().numpy(),
+                np.array([st[_lib.ST_CGT]]),
+                np.array([st[_lib.ST_PR], st[_lib.ST_DR], st[_lib.ST_GAP]])]
+
+    # algorithmic traffic model used by bench.py for the roofline
+    def bytes_model(self) -> dict:
+        n, m = self.n, self.m
+        N = n + m + 1
+        fwd, adj = self.dev.algo_bytes(False), self.dev.algo_bytes(True)
+        cg_iter = (fwd + 8 * 2 * n) + (adj + 8 * 2 * n) + 8 * 6 * n
+        outer = (2 * adj + 8 * 4 * n) + (fwd + 8 * 3 * m) + 8 * (8 * N)
+        check = fwd + adj + 8 * 4 * m + 8 * 2 * n
+        return {"per_cg_iter": cg_iter, "per_iter": outer, "per_check": check}
+
+
+def build_scs_graph(problem: ConeProblem, settings: ScsSettings | None = None) -> SolverPlan:
+    """Compile the solver for ``problem`` (setup solve included; scs.py:433-469)."""
+    settings = settings or ScsSettings()
+    return SolverPlan(problem, settings)
+
+
+def iterate_states(graph: SolverPlan, max_iters: int) -> Iterator[tuple[int, list]]:
+    """Step the solver one splitting iteration at a time (scs.py:482-494).
+
+    Yields (iteration, loop-variable list [u, v, k, since, status, cgw, cgt,
+    resid]) after each iteration; every step is one device launch running
+    exactly one iteration with the residual triple evaluated.
+    """
+    graph.reset()
+    k = 0
+    state = graph.loop_vars()
+    while k < max_iters and state[_ISTATUS][0] == _STATUS_RUNNING:
+        graph.run(1, resid_every_iter=True)
+        k += 1
+        state = graph.loop_vars()
+        yield k, state
+
+
+def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.ndarray,
+              iterations: int, cg_total: float) -> ScsSolution:
+    """scs.py:497-538."""
+    A, b, c = problem.A, problem.b, problem.c
+    n, m = A.cols, A.rows
+    tau, kappa = float(u[-1]), float(v[-1])
+    ux, uy, vs = u[:n], u[n:n + m], v[n:n + m]
+    avg_cg = cg_total / iterations if iterations > 0 else 0.0
+    nan_n, nan_m = np.full(n, np.nan), np.full(m, np.nan)
+    eps = settings.eps
+    if tau > SMALL_TAU:
+        x, y, s = ux / tau, uy / tau, vs / tau
+        pr, dr, gap = residuals(ScsIterate(u, v), problem)
+        pobj, dobj = float(c @ x), -float(b @ y)
+        if max(pr, dr, gap) <= eps:
+            return ScsSolution(SOLVED, x, y, s, pobj, dobj, pr, dr, gap, iterations, avg_cg)
+    else:
+        pr = dr = gap = np.inf
+        x = y = s = None
+    den_i = -float(b @ uy)
+    if den_i > 0:
+        res_i = float(np.linalg.norm(A.adjoint_apply(uy))) / den_i
+        if tau < settings.cert_tau_ratio * max(kappa, 1.0) and res_i <= eps:
+            return ScsSolution(INFEASIBLE, nan_n, uy / den_i, nan_m, np.nan, np.nan,
+                               np.inf, res_i, np.inf, iterations, avg_cg)
+    den_u = -float(c @ ux)
+    if den_u > 0:
+        res_u = float(np.linalg.norm(A.forward(ux) + vs)) / den_u
+        if tau < settings.cert_tau_ratio * max(kappa, 1.0) and res_u <= eps:
+            return ScsSolution(UNBOUNDED, ux / den_u, nan_m, vs / den_u, np.nan, np.nan,
+                               res_u, np.inf, np.inf, iterations, avg_cg)
+    if x is None:
+        return ScsSolution(MAX_ITERS, nan_n, nan_m, nan_m, np.nan, np.nan, pr, dr, gap,
+                           iterations, avg_cg)
+    status = INACCURATE if max(pr, dr, gap) <= 10.0 * eps else MAX_ITERS
+    return ScsSolution(status, x, y, s, float(c @ x), -float(b @ y), pr, dr, gap,
+                       iterations, avg_cg)
+
+
+def solve_built(problem: ConeProblem, settings: ScsSettings, graph: SolverPlan,
+                trace_path=None) -> ScsSolution:
+    """Run a compiled solver to termination (scs.py:541-568)."""
+    if trace_path is None:
+        graph.reset()
+        graph.run(settings.max_iters)
+        st = graph.state()
+        u = graph.buf["u"].cpu().numpy()
+        v = graph.buf["v"].cpu().numpy()
+        return _classify(problem, settings, u, v, int(st[_lib.ST_K]), float(st[_lib.ST_CGT]))
+    prev_cg = 0.0
+    state = graph.loop_vars()
+    with open(trace_path, "w") as fh:
+        for k, state in iterate_states(graph, settings.max_iters):
+            cg_now = float(state[_ICGT][0])
+            pr, dr, gp = state[_IRESID]
+            fh.write(json.dumps({"iteration": k, "primal": float(pr), "dual": float(dr),
+                                 "gap": float(gp), "cg_iters": int(cg_now - prev_cg)}) + "\n")
+            prev_cg = cg_now
+    u, v = state[_IU], state[_IV]
+    return _classify(problem, settings, u, v, int(state[_IK][0]), float(state[_ICGT][0]))
+
+
+def solve(problem: ConeProblem, settings: ScsSettings | None = None,
+          trace_path=None) -> ScsSolution:
+    """Build the solver for ``problem`` and run it to termination (scs.py:571-576)."""
+    settings = settings or ScsSettings()
+    graph = build_scs_graph(problem, settings)
+    return solve_built(problem, settings, graph, trace_path)

@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path vs the reference's golden vectors and the oracle.
+
+Every test here calls through the C ABI (libcgb200.so via ctypes) on a
+B200.  Tolerances (north star): operator applies and cone projections to
+1e-12 relative (only summation order differs), CG iteration counts within
+one step, SCS status identical, iteration counts within +-2% (or one
+check interval for short runs), objective within 1e-6 relative at
+convergence, residuals <= eps.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_1609_03488_b200 as pkg
+from paper_1609_03488_b200 import cg, cones, linop, scs
+from _golden import build_cones, build_tree, load, scs_case_names
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib_loaded():
+    from paper_1609_03488_b200 import _lib
+    return _lib.load_library()
+
+
+def test_library_is_the_native_path():
+    lib = _lib_loaded()
+    assert lib.cgb_abi_version() == 1
+    from paper_1609_03488_b200 import _lib
+    ctx = _lib.device_context()
+    sms, per_sm, threads = ctx.geometry()
+    assert sms >= 100 and per_sm >= 1 and threads >= 128
+
+
+def test_linop_cases_match_reference():
+    data, meta = load("linop_cases")
+    for i, case in enumerate(meta["cases"]):
+        op = linop.Operator(build_tree(case["tree"], data, linop))
+        ax = op.forward(data[case["x"]])
+        aty = op.adjoint_apply(data[case["y"]])
+        sx = 1.0 + np.abs(data[case["ax"]]).max(initial=0)
+        sy = 1.0 + np.abs(data[case["aty"]]).max(initial=0)
+        np.testing.assert_allclose(ax, data[case["ax"]], rtol=1e-11, atol=1e-11 * sx,
+                                   err_msg=f"case {i} forward")
+        np.testing.assert_allclose(aty, data[case["aty"]], rtol=1e-11, atol=1e-11 * sy,
+                                   err_msg=f"case {i} adjoint")
+        assert linop.nnz_estimate(op) == case["nnz"]
+
+
+def test_adjoint_identity_random():
+    rng = np.random.default_rng(5)
+    data, meta = load("linop_cases")
+    for case in meta["cases"]:
+        op = linop.Operator(build_tree(case["tree"], data, linop))
+        x = rng.standard_normal(op.cols)
+        y = rng.standard_normal(op.rows)
+        ax, aty = op.forward(x), op.adjoint_apply(y)
+        assert abs(ax @ y - x @ aty) <= 1e-10 * (1.0 + np.linalg.norm(ax) * np.linalg.norm(y))
+
+
+def test_conv_by_hand_and_large():
+    op = linop.conv1d([1.0, 1.0], 2)
+    np.testing.assert_allclose(op.forward(np.array([1.0, 2.0])), [1.0, 3.0, 2.0])
+    np.testing.assert_allclose(op.adjoint_apply(np.array([1.0, 3.0, 2.0])), [4.0, 5.0])
+    from oracle import linop_ref
+    rng = np.random.default_rng(1)
+    for k, n in [(101, 100_000), (7, 33), (600, 550)]:
+        c = rng.standard_normal(k)
+        x = rng.standard_normal(n)
+        y = rng.standard_normal(n + k - 1)
+        op = linop.conv1d(c, n)
+        f = op.forward(x)
+        np.testing.assert_allclose(f, linop_ref.conv_full(c, x, "direct"), rtol=1e-10,
+                                   atol=1e-11 * np.abs(f).max())
+        a = op.adjoint_apply(y)
+        np.testing.assert_allclose(a, linop_ref.corr_valid(c, y, "direct"), rtol=1e-10,
+                                   atol=1e-11 * np.abs(a).max())
+
+
+def test_conv2d_against_oracle():
+    from oracle import linop_ref
+    import _exprs as E
+    rng = np.random.default_rng(2)
+    for (h, w, kh, kw) in [(7, 5, 3, 3), (40, 33, 15, 15), (64, 64, 1, 5)]:
+        K = rng.standard_normal((kh, kw))
+        op = linop.conv2d(K, (h, w))
+        ref = E.Conv2D(K, (h, w))
+        x = rng.standard_normal(h * w)
+        y = rng.standard_normal(op.rows)
+        np.testing.assert_allclose(op.forward(x), linop_ref.forward(ref, x), rtol=1e-10,
+                                   atol=1e-10)
+        np.testing.assert_allclose(op.adjoint_apply(y), linop_ref.adjoint(ref, y), rtol=1e-10,
+                                   atol=1e-10)
+
+
+def test_cone_cases_match_reference():
+    data, meta = load("cone_cases")
+    for j, (kind, dim) in enumerate(meta["cones"]):
+        cone = getattr(cones, kind)(dim)
+        V, P = data[f"v{j}"], data[f"p{j}"]
+        K = cones.ConeProduct([cone] * len(V))
+        out = cones.project_product(K, V.reshape(-1)).reshape(V.shape)
+        np.testing.assert_allclose(out, P, rtol=1e-13, atol=1e-13)
+        if kind != "ZeroCone":
+            outd = cones.project_product_dual(K, V.reshape(-1)).reshape(V.shape)
+            np.testing.assert_allclose(outd, P, rtol=1e-13, atol=1e-13)
+        else:
+            np.testing.assert_array_equal(cones.project_product_dual(K, V.reshape(-1)),
+                                          V.reshape(-1))
+
+
+def test_large_soc_grid_reduction():
+    from oracle import cones_ref
+    import _exprs as E
+    rng = np.random.default_rng(3)
+    for dim in (5000, 300_001):
+        v = rng.standard_normal(dim)
+        for t0 in (0.0, 1e4, -1e4, np.linalg.norm(v[1:])):
+            v[0] = t0
+            got = cones.project(cones.SecondOrderCone(dim), v)
+            want = cones_ref.project_cone(E.SecondOrderCone(dim), v)
+            np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_cg_cases_match_reference():
+    data, meta = load("cg_cases")
+    for case in meta["cases"]:
+        A = linop.Operator(build_tree(case["tree"], data, linop))
+        b = data[case["b"]]
+        rec = cg.operator_recipe(A) if case["recipe"] == "direct" else \
+            cg.make_normal_operator(A, case["lam"])
+        res = cg.cg_solve(cg.CgSpec(rec, b, np.zeros(len(b)), tol=case["tol"]))
+        assert res.converged == case["converged"]
+        assert abs(res.iterations - case["iters"]) <= 1
+        ref = data[case["x"]]
+        assert np.linalg.norm(res.x - ref) <= 1e-7 * np.linalg.norm(ref)
+
+
+def test_cg_edge_cases():
+    res = cg.cg_solve(cg.CgSpec(cg.operator_recipe(linop.identity(4)), np.zeros(4), np.zeros(4)))
+    assert res.iterations == 0 and res.converged and res.final_residual_norm == 0.0
+    b = np.array([3.0, -1.0, 2.0])
+    res = cg.cg_solve(cg.CgSpec(cg.operator_recipe(linop.identity(3)), b, np.zeros(3)))
+    np.testing.assert_allclose(res.x, b, atol=1e-14)
+    assert res.iterations == 1
+    rng = np.random.default_rng(6)
+    M = rng.standard_normal((40, 40))
+    Ad = M.T @ M + np.eye(40)
+    res = cg.cg_solve(cg.CgSpec(cg.operator_recipe(linop.dense(Ad)), rng.standard_normal(40),
+                                np.zeros(40), max_iter=2))
+    assert not res.converged and res.iterations == 2
+
+
+def test_subspace_cases_match_reference():
+    data, meta = load("subspace_cases")
+    for i, case in enumerate(meta["cases"]):
+        A = linop.dense(data[f"A{i}"])
+        prob = scs.ConeProblem(A, data[f"b{i}"], data[f"c{i}"],
+                               cones.ConeProduct([cones.NonNegCone(case["m"])]))
+        cached = scs.prepare_subspace(prob)
+        np.testing.assert_allclose(cached.g, data[f"g{i}"], rtol=1e-9, atol=1e-11)
+        out = scs.subspace_project(data[f"w{i}"], cached)
+        np.testing.assert_allclose(out, data[f"out{i}"], rtol=1e-8, atol=1e-10)
+
+
+def _problem(data, meta):
+    A = linop.Operator(build_tree(meta["tree"], data, linop))
+    K = cones.ConeProduct(build_cones(meta["cones"], cones))
+    return scs.ConeProblem(A, np.array(data["b"]), np.array(data["c"]), K)
+
+
+def _settings(meta):
+    return scs.ScsSettings(**meta["settings"])
+
+
+@pytest.mark.parametrize("name", scs_case_names())
+def test_scs_trace_matches_reference(name):
+    data, meta = load(name)
+    prob = _problem(data, meta)
+    graph = scs.build_scs_graph(prob, _settings(meta))
+    assert abs(graph.cached.denom - meta["denom"]) <= 1e-9 * abs(meta["denom"])
+    tu, tv, tcg = data["trace_u"], data["trace_v"], data["trace_cgt"]
+    for k, state in scs.iterate_states(graph, min(len(tu), 10)):
+        su = 1.0 + np.linalg.norm(tu[k - 1])
+        assert np.linalg.norm(state[0] - tu[k - 1]) <= 1e-7 * su, f"u at iteration {k}"
+        sv = 1.0 + np.linalg.norm(tv[k - 1])
+        assert np.linalg.norm(state[1] - tv[k - 1]) <= 1e-7 * sv, f"v at iteration {k}"
+        assert abs(state[6][0] - tcg[k - 1]) <= 1
+
+
+@pytest.mark.parametrize("name", scs_case_names())
+def test_scs_solve_matches_reference(name):
+    data, meta = load(name)
+    prob = _problem(data, meta)
+    st = _settings(meta)
+    sol = scs.solve(prob, st)
+    assert sol.status == meta["status"], (sol.status, sol.iterations, meta["iterations"])
+    it_ref = meta["iterations"]
+    slack = max(0.02 * it_ref, st.check_interval)
+    assert abs(sol.iterations - it_ref) <= slack, (sol.iterations, it_ref)
+    if sol.status == "solved":
+        assert max(sol.primal_residual, sol.dual_residual, sol.gap) <= st.eps
+        assert abs(sol.pobj - meta["pobj"]) <= 1e-6 * (1.0 + abs(meta["pobj"])) + 10 * st.eps * abs(meta["pobj"])
+    if sol.status == "infeasible":
+        y = sol.y
+        assert np.all(y >= -1e-8)
+        np.testing.assert_allclose(prob.b @ y, -1.0, atol=1e-9)
+    if sol.status == "unbounded":
+        np.testing.assert_allclose(prob.c @ sol.x, -1.0, atol=1e-9)
+
+
+def test_scs_matches_oracle_exactly_on_lasso():
+    """Same inputs through oracle and device: same iterations, same objective."""
+    from oracle import scs_ref
+    import _exprs as E
+    data, meta = load("scs_lasso_dense_30_7")
+    prob = _problem(data, meta)
+    st = _settings(meta)
+    sol = scs.solve(prob, st)
+    oprob = E.Problem(build_tree(meta["tree"], data, E), np.array(data["b"]),
+                      np.array(data["c"]), E.ConeProduct(build_cones(meta["cones"], E)))
+    osol, _ = scs_ref.scs_solve(oprob, scs_ref.ScsOracleSettings(**meta["settings"]))
+    assert sol.iterations == osol.iterations
+    assert abs(sol.pobj - osol.pobj) <= 1e-6 * abs(osol.pobj)
+
+
+def test_trace_file_round_trip(tmp_path):
+    prob = scs.ConeProblem(linop.dense([[-1.0]]), np.array([-1.0]), np.array([1.0]),
+                           cones.ConeProduct([cones.NonNegCone(1)]))
+    settings = scs.ScsSettings(eps=1e-6, max_iters=2000)
+    path = tmp_path / "trace.jsonl"
+    graph = scs.build_scs_graph(prob, settings)
+    sol = scs.solve_built(prob, settings, graph, trace_path=path)
+    records = [json.loads(line) for line in path.read_text().splitlines()]
+    assert len(records) == sol.iterations
+    sol2 = scs.solve_built(prob, settings, graph)
+    assert sol2.iterations == sol.iterations
+    np.testing.assert_array_equal(sol2.x, sol.x)
+
+
+def test_cone_step_orthogonality():
+    rng = np.random.default_rng(11)
+    n, m = 4, 6
+    Ad = rng.standard_normal((m, n))
+    x0 = rng.standard_normal(n)
+    s0 = np.abs(rng.standard_normal(m)) + 0.1
+    y0 = np.abs(rng.standard_normal(m)) + 0.1
+    prob = scs.ConeProblem(linop.dense(Ad), Ad @ x0 + s0, -Ad.T @ y0,
+                           cones.ConeProduct([cones.NonNegCone(m)]))
+    graph = scs.build_scs_graph(prob, scs.ScsSettings(eps=1e-9, max_iters=100))
+    for _, state in scs.iterate_states(graph, 100):
+        u, v = state[0], state[1]
+        assert abs(u @ v) / (1.0 + np.linalg.norm(u) * np.linalg.norm(v)) <= 1e-9
+
+
+def test_deconv_short_kernel_end_to_end():
+    """North-star shape at small scale: n=20000, k=101 vs the oracle."""
+    from oracle import scs_ref
+    import _exprs as E
+    from paper_1609_03488_b200 import canon
+    n, k = 20_000, 101
+    c, b, _ = canon.gen_deconv1d(n, k, seed=3, spikes=20)
+    prob = canon.build_deconv(canon.DeconvProblem(c, b, n=n))
+    assert prob.dims == (n + 1, 2 * n + k)
+    st = scs.ScsSettings(eps=1e-3, max_iters=3000)
+    sol = scs.solve(prob, st)
+    C = E.Conv1D(c, n)
+    stuffed = E.VStack([E.AdjointOf(E.VStack([E.Identity(n), E.ZeroOp(1, n)])),
+                        E.AdjointOf(E.VStack([E.ZeroOp(n, 1), E.Identity(1)])),
+                        E.AdjointOf(E.VStack([E.AdjointOf(C), E.ZeroOp(1, n + k - 1)]))])
+    oprob = E.Problem(E.Scale(-1.0, stuffed), prob.b, prob.c,
+                      E.ConeProduct([E.NonNegCone(n), E.SecondOrderCone(n + k)]))
+    osol, _ = scs_ref.scs_solve(oprob, scs_ref.ScsOracleSettings(eps=1e-3, max_iters=3000))
+    assert sol.status == osol.status
+    assert abs(sol.iterations - osol.iterations) <= max(0.02 * osol.iterations, 20)
+    if sol.status == "solved":
+        assert abs(sol.pobj - osol.pobj) <= 1e-6 * abs(osol.pobj) + 1e-3 * abs(osol.pobj)
