@@ -163,13 +163,17 @@ typedef struct cgb_scs_problem {
   double dr_scale;     /* 1 / (1 + ||c||)                                    */
 } cgb_scs_problem;
 
-/* Device buffers owned by the caller.  N = n + m + 1. */
+/* Device buffers owned by the caller.  N = n + m + 1.
+ * Invariant of the embedding: v = (0, s, kappa) -- the x block of v is zero
+ * on entry (cgb_scs_run keeps it zero and never reads it).  u is written on
+ * check iterations (and on the last iteration a call can run); between them
+ * only u's tau entry is current.  p1 and q are reserved (unused). */
 typedef struct cgb_scs_work {
   double* u; double* v; double* w;   /* N each; w = u + v maintained          */
   double* cgx;                        /* n : CG warm start (p1 of last iter)   */
   double* tax;                        /* m : A cgx, tracked through CG updates */
   double* gx;                         /* n : A^T A cgx, tracked likewise       */
-  double* r; double* p0; double* p1; double* q;  /* n each : CG vectors        */
+  double* r; double* p0; double* p1; double* q;  /* n each : CG r, p (p0)      */
   double* t;                          /* m : A p scratch                       */
   double* state;                      /* CGB_STATE_LEN doubles, see below      */
 } cgb_scs_work;
@@ -205,6 +209,12 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
 int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const double* d2,
                     double* z, double tol, int64_t max_iter, const double* c, const double* b,
                     double* scratch, cgb_cg_result* res, double* hdot, void* stream);
+
+/* Phase profiler: when dev_acc != NULL, later cgb_scs_run calls on this ctx
+ * add the nanoseconds spent in each phase to dev_acc[0..7] (device
+ * memory): 0 subspace rhs, 1 CG t = A p, 2 CG A^T t + updates, 3 cone pass
+ * A, 4 cone pass B, 5 residual check, 6 per-launch setup.  NULL disables. */
+int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc);
 
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Run `iters` grid barriers (mode 0) or grid reductions (mode 1) in one

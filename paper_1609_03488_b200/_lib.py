@@ -98,6 +98,7 @@ SIGNATURES = {
     "cgb_inner_solve": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _f64, _i64, _vp, _vp, _vp,
                                        ctypes.POINTER(CgResult), ctypes.POINTER(_f64), _vp]),
     "cgb_debug_barrier": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp]),
+    "cgb_scs_profile": (ctypes.c_int, [_vp, _vp]),
 }
 
 

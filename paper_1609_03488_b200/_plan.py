@@ -60,7 +60,7 @@ class _Builder:
         self.temp_len: list[int] = []
         self.temp_level: list[int] = []
         self.keep: list = []
-        self.algo_bytes = 0  # algorithmic bytes of one application (roofline)
+        self.leaf_nnz: dict[int, int] = {}  # CSR leaf index -> nnz (roofline bytes)
 
     # -- leaves -------------------------------------------------------------
     def _add_leaf(self, key, make):
@@ -108,6 +108,7 @@ class _Builder:
                 p, i, v = buf[key]
                 self.keep.extend((p, i, v))
                 rows, cols = (e.cols, e.rows) if adj else (e.rows, e.cols)
+                self.leaf_nnz[len(self.leaves)] = int(e.matrix.nnz)
                 return _lib.Leaf(kind=_lib.LEAF_CSR, rows=rows, cols=cols, val=v.data_ptr(),
                                  rowptr=p.data_ptr(), colidx=i.data_ptr()), 0
             return self._add_leaf((id(e), adj), make)
@@ -270,17 +271,17 @@ class _Builder:
         return desc
 
 
-def _leaf_algo_bytes(leaf: _lib.Leaf) -> int:
-    """Compulsory HBM bytes of one leaf application (read operands once)."""
+def _leaf_data_bytes(leaf: _lib.Leaf, nnz: int) -> int:
+    """Compulsory HBM bytes of a leaf's own data (matrix values / indices)."""
     k = leaf.kind
-    if k == _lib.LEAF_IDENTITY:
-        return 8 * leaf.rows
     if k == _lib.LEAF_DENSE:
-        return 8 * leaf.rows * leaf.cols + 8 * leaf.cols
+        return 8 * leaf.rows * leaf.cols
     if k == _lib.LEAF_CSR:
-        return 0  # filled by caller from nnz
-    if k in (_lib.LEAF_CONV1D, _lib.LEAF_CORR1D, _lib.LEAF_CONV2D, _lib.LEAF_CORR2D):
-        return 8 * leaf.cols
+        return 12 * nnz + 8 * (leaf.rows + 1)
+    if k in (_lib.LEAF_CONV1D, _lib.LEAF_CORR1D):
+        return 8 * leaf.k0
+    if k in (_lib.LEAF_CONV2D, _lib.LEAF_CORR2D):
+        return 8 * leaf.k0 * leaf.k1
     return 0
 
 
@@ -336,9 +337,7 @@ class DeviceOp:
     def algo_bytes(self, adjoint: bool = False) -> int:
         """Compulsory bytes of one application: operand reads + output write."""
         b = self.adj if adjoint else self.fwd
-        total = 0
-        for t in b.terms:
-            leaf = b.leaves[t[0]]
-            total += _leaf_algo_bytes(leaf)
-        n_out = self.cols if adjoint else self.rows
-        return total + 8 * n_out + 8 * sum(b.temp_len) * 2
+        total = sum(_leaf_data_bytes(leaf, b.leaf_nnz.get(i, 0))
+                    for i, leaf in enumerate(b.leaves))
+        n_in, n_out = (self.rows, self.cols) if adjoint else (self.cols, self.rows)
+        return total + 8 * n_in + 8 * n_out + 16 * sum(b.temp_len)

@@ -35,7 +35,7 @@ namespace {
 
 struct EpiStore {  // y -> out
   double* out;
-  __device__ void tile(int64_t row, int R, int left, const double (&y)[CGB_RC], double*) const {
+  __device__ void tile(int64_t row, int64_t jlo, int R, int left, const double (&y)[CGB_RC], double*) const {
 #pragma unroll
     for (int r = 0; r < CGB_RC; ++r)
       if (CGB_EPI_VALID(r)) out[row + 32 * r] = y[r];
@@ -43,48 +43,50 @@ struct EpiStore {  // y -> out
 };
 
 // Splitting-step / inner-solve start: with y = A^T d2 and g = A^T A x0,
-//   rhs = d1 - y ;  r = rhs - (x0 + g) ;  p = r ;  sums: rhs.rhs, r.r
+//   rhs = d1 - y ;  r = rhs - (x0 + g) ;  sums: rhs.rhs, r.r (+ c.x0)
 // (scs.py:349 rhs = wz1 - A^T wz2 ; cg.py:129 r0 = b - (1*x + A^T A x))
 struct EpiRhs {
   const double* d1;
   const double* x0;
   const double* g;
+  const double* c;  // optional: slot 2 gets c.x0
   double* r;
-  double* p;
-  __device__ void tile(int64_t j, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
-    double a[CGB_RC], x[CGB_RC], gg[CGB_RC];
+    double a[CGB_RC], x[CGB_RC], gg[CGB_RC], cc[CGB_RC];
 #pragma unroll
-    for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) { a[q] = d1[j + 32 * q]; x[q] = x0[j + 32 * q]; gg[q] = g[j + 32 * q]; }
+    for (int q = 0; q < CGB_RC; ++q) {
+      const int64_t jq = CGB_EPI_IDX(j, q);
+      a[q] = d1[jq]; x[q] = x0[jq]; gg[q] = g[jq];
+      if (c) cc[q] = c[jq];
+    }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
         const double rhs = a[q] - y[q];
         const double rr = rhs - (x[q] + gg[q]);
         r[j + 32 * q] = rr;
-        p[j + 32 * q] = rr;
         part[0] += rhs * rhs;
         part[1] += rr * rr;
+        if (c) part[2] += cc[q] * x[q];
       }
     }
   }
 };
 
-// standalone CG init: r = b - apply(x), p = r ; sums r.r, b.b   (cg.py:129-132)
+// standalone CG init: r = b - apply(x) ; sums r.r, b.b   (cg.py:129-132)
 struct EpiR0 {
   const double* b;
   const double* x;
   double* r;
-  double* p;
   double lam;
   int normal;
-  __device__ void tile(int64_t j, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double bb[CGB_RC], xx[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) { bb[q] = b[j + 32 * q]; xx[q] = x[j + 32 * q]; }
+      { const int64_t jq = CGB_EPI_IDX(j, q); bb[q] = b[jq]; xx[q] = x[jq]; }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
@@ -92,31 +94,8 @@ struct EpiR0 {
         if (normal && lam != 0.0) ax = lam * xx[q] + y[q];
         const double rr = bb[q] - ax;
         r[j + 32 * q] = rr;
-        p[j + 32 * q] = rr;
         part[0] += rr * rr;
         part[1] += bb[q] * bb[q];
-      }
-    }
-  }
-};
-
-// CG phase B (normal recipe): q = lam p + A^T t ; sum p.q   (cg.py:80-83,111)
-struct EpiQ {
-  const double* p;
-  double* qv;
-  double lam;
-  __device__ void tile(int64_t j, int R, int left, const double (&y)[CGB_RC],
-                       double* part) const {
-    double pp[CGB_RC];
-#pragma unroll
-    for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) pp[q] = p[j + 32 * q];
-#pragma unroll
-    for (int q = 0; q < CGB_RC; ++q) {
-      if (CGB_EPI_VALID(q)) {
-        const double qj = (lam != 0.0) ? lam * pp[q] + y[q] : y[q];
-        qv[j + 32 * q] = qj;
-        part[0] += pp[q] * qj;
       }
     }
   }
@@ -126,12 +105,12 @@ struct EpiQ {
 struct EpiQDirect {
   InVec pin;
   double* qv;
-  __device__ void tile(int64_t j, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double pp[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) pp[q] = pin(j + 32 * q);
+      pp[q] = pin(CGB_EPI_IDX(j, q));
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
@@ -148,12 +127,12 @@ struct EpiZ2 {
   double* z2;
   const double* d2;
   const double* b;
-  __device__ void tile(int64_t i, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double dd[CGB_RC], bb[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) { dd[q] = d2[i + 32 * q]; bb[q] = b ? b[i + 32 * q] : 0.0; }
+      { const int64_t iq = CGB_EPI_IDX(i, q); dd[q] = d2[iq]; bb[q] = b ? b[iq] : 0.0; }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
@@ -171,12 +150,12 @@ struct EpiRawP {
   const double* s;
   const double* b;
   double utau;
-  __device__ void tile(int64_t i, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double ss[CGB_RC], bb[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) { ss[q] = s[i + 32 * q]; bb[q] = b[i + 32 * q]; }
+      { const int64_t iq = CGB_EPI_IDX(i, q); ss[q] = s[iq]; bb[q] = b[iq]; }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
@@ -193,12 +172,12 @@ struct EpiRawP {
 struct EpiRawD {
   const double* c;
   double utau;
-  __device__ void tile(int64_t j, int R, int left, const double (&y)[CGB_RC],
+  __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double cc[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q)
-      if (CGB_EPI_VALID(q)) cc[q] = c[j + 32 * q];
+      cc[q] = c[CGB_EPI_IDX(j, q)];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
@@ -212,118 +191,219 @@ struct EpiRawD {
 };
 
 // ===========================================================================
+// phase profiler (optional): block 0 / thread 0 accumulates globaltimer
+// deltas per phase; every mark sits right after a grid barrier, so the
+// delta is the whole grid's time in that phase.
+// ===========================================================================
+enum ProfPhase : int {
+  PROF_RHS = 0,     // subspace rhs: A^T w_y + r0 + reduce
+  PROF_CG_F = 1,    // CG: t = A p + reduce
+  PROF_CG_A = 2,    // CG: A^T t + fused updates + reduce
+  PROF_CONE_A = 3,  // cone pass A (+ large-SOC reduce)
+  PROF_CONE_B = 4,  // cone pass B + barrier
+  PROF_CHECK = 5,   // residual check
+  PROF_INIT = 6,    // per-launch setup (b.Ax, b.w_y)
+  PROF_N = 8
+};
+
+struct Prof {
+  double* acc;  // PROF_N doubles (ns), or null
+  uint64_t last;
+  __device__ explicit Prof(double* p) : acc(p), last(0) {
+    if (acc && blockIdx.x == 0 && threadIdx.x == 0) last = globaltimer();
+  }
+  __device__ __forceinline__ void mark(int phase) {
+    if (acc && blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint64_t now = globaltimer();
+      acc[phase] += (double)(now - last);
+      last = now;
+    }
+  }
+};
+
+// ===========================================================================
 // CG loop shared by k_cg, k_inner and k_scs  (cg.py:87-137)
 // ===========================================================================
-// Optional incremental tracking (splitting solver): ax = A x and gx = A^T A x
-// follow x through the updates x += alpha p (ax += alpha A p, gx += alpha
-// (q - p)), so the next splitting step needs neither A x nor A^T A x anew.
-// With track, phase C also accumulates h.(x, wy + ax) for tau~ (scs.py:357).
+// Two grid reductions per iteration.
+// Normal recipe, solve (lam I + A^T A) x = b:
+//   phase F : t = A p, p = r + beta p_old read through the fused accessor;
+//             sums t.t and p.p (+ c.p, b.t when tracking), then
+//             alpha = rns / (lam p.p + t.t)       [= rns / p.(lam p + A^T A p)]
+//   phase A : y = A^T t; per element p = r + beta p_old (stored in place),
+//             q = lam p + y, x += alpha p, r -= alpha q, gx += alpha y;
+//             sum r.r ; ax += alpha t when tracking
+// Direct recipe (A square SPD): phase F q = A p, sum p.q; phase U the
+// stream update.  Same updates as the reference listing, reassociated
+// only in how p.Ap is summed.
 struct CgBufs {
   double* x;
   double* r;
-  double* pb[2];  // pb[0] holds r0 on entry
-  double* q;
-  double* t;      // m scratch (normal recipe): A p
-  double* ax;     // m, tracked A x (or null)
-  double* gx;     // n, tracked A^T A x (or null)
-  const double* wy;  // m: wz2 for h.p (with tracking)
-  const double* b;   // m
-  const double* c;   // n
+  double* p;   // direction, updated in place
+  double* q;   // direct recipe only
+  double* t;   // m scratch (normal recipe): A p
+  double* ax;  // m, tracked A x (or null)
+  double* gx;  // n, tracked A^T A x (or null)
+  const double* b;  // m, tracking dots (or null)
+  const double* c;  // n, tracking dots (or null)
 };
 
-struct PNew {  // p_new = r + beta p_old
-  const double* r; const double* po; double* pn; double beta;
-  double rv[CGB_U], pv[CGB_U];
-  __device__ void load(int64_t i, int u) { rv[u] = r[i]; pv[u] = po[i]; }
-  __device__ void compute(int64_t i, int u) { pn[i] = rv[u] + beta * pv[u]; }
-};
-
-struct CgUpdateN {  // x += alpha p ; r -= alpha q ; gx += alpha (q - p)
-  double* x; double* r; const double* p; const double* q; double* gx; const double* c;
-  double alpha;
-  double rr, hc;
-  double xv[CGB_U], rv[CGB_U], pv[CGB_U], qv[CGB_U], gv[CGB_U], cv[CGB_U];
-  __device__ void load(int64_t i, int u) {
-    xv[u] = x[i]; rv[u] = r[i]; pv[u] = p[i]; qv[u] = q[i];
-    if (gx) { gv[u] = gx[i]; cv[u] = c[i]; }
-  }
-  __device__ void compute(int64_t i, int u) {
-    const double xn = xv[u] + alpha * pv[u];
-    x[i] = xn;
-    const double ri = rv[u] - alpha * qv[u];
-    r[i] = ri;
-    rr += ri * ri;
-    if (gx) {
-      gx[i] = gv[u] + alpha * (qv[u] - pv[u]);
-      hc += cv[u] * xn;
+// phase F (normal): t = A p ; sums t.t (slot 0), b.t (slot 3)
+struct EpiT {
+  double* t;
+  const double* b;
+  __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
+                       double* part) const {
+    double bb[CGB_RC];
+    if (b) {
+#pragma unroll
+      for (int q = 0; q < CGB_RC; ++q)
+        bb[q] = b[CGB_EPI_IDX(i, q)];
+    }
+#pragma unroll
+    for (int q = 0; q < CGB_RC; ++q) {
+      if (CGB_EPI_VALID(q)) {
+        t[i + 32 * q] = y[q];
+        part[0] += y[q] * y[q];
+        if (b) part[3] += bb[q] * y[q];
+      }
     }
   }
 };
 
-struct CgUpdateM {  // ax += alpha t ; sum b.(wy + ax)
-  double* ax; const double* t; const double* wy; const double* b; double alpha;
-  double hb;
-  double av[CGB_U], tv[CGB_U], wv[CGB_U], bv[CGB_U];
-  __device__ void load(int64_t i, int u) { av[u] = ax[i]; tv[u] = t[i]; wv[u] = wy[i]; bv[u] = b[i]; }
-  __device__ void compute(int64_t i, int u) {
-    const double an = av[u] + alpha * tv[u];
-    ax[i] = an;
-    hb += bv[u] * (wv[u] + an);
+// phase F stream: p = pin(i) ; sums p.p (slot 1), c.p (slot 2)
+struct PDots {
+  InVec pin;
+  const double* c;
+  double pp, cp;
+  double pv[CGB_U], cv[CGB_U];
+  __device__ void load(int64_t i, int u) {
+    pv[u] = pin(i);
+    if (c) cv[u] = c[i];
+  }
+  __device__ void compute(int64_t, int u) {
+    pp += pv[u] * pv[u];
+    if (c) cp += cv[u] * pv[u];
   }
 };
 
-// Runs CG from the state prepared by the caller (r = b - apply(x),
-// pb[0] = r, rns = r.r).  Returns the iteration count; `hp` receives the
-// tracked h.p of the final iterate when tracking is on.
+// phase A (normal): the whole CG update in the A^T t epilogue ; sum r.r
+struct EpiCgUpd {
+  double* r; double* p; double* x; double* gx;
+  double beta; int first; double lam, alpha;
+  __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
+                       double* part) const {
+    double rv[CGB_RC], pv[CGB_RC], xv[CGB_RC], gv[CGB_RC];
+#pragma unroll
+    for (int q = 0; q < CGB_RC; ++q) {
+      const int64_t jq = CGB_EPI_IDX(j, q);
+      rv[q] = r[jq];
+      if (!first) pv[q] = p[jq];
+      xv[q] = x[jq];
+      if (gx) gv[q] = gx[jq];
+    }
+#pragma unroll
+    for (int q = 0; q < CGB_RC; ++q) {
+      if (CGB_EPI_VALID(q)) {
+        const double pp = first ? rv[q] : rv[q] + beta * pv[q];
+        const double qq = (lam != 0.0) ? lam * pp + y[q] : y[q];
+        const double rn = rv[q] - alpha * qq;
+        p[j + 32 * q] = pp;
+        x[j + 32 * q] = xv[q] + alpha * pp;
+        r[j + 32 * q] = rn;
+        if (gx) gx[j + 32 * q] = gv[q] + alpha * y[q];
+        part[0] += rn * rn;
+      }
+    }
+  }
+};
+
+struct AxUpd {  // ax += alpha t
+  double* ax; const double* t; double alpha;
+  double av[CGB_U], tv[CGB_U];
+  __device__ void load(int64_t i, int u) { av[u] = ax[i]; tv[u] = t[i]; }
+  __device__ void compute(int64_t i, int u) { ax[i] = av[u] + alpha * tv[u]; }
+};
+
+// direct recipe phase U: p = r + beta p ; x += alpha p ; r -= alpha q ; sum r.r
+struct CgUpdDirect {
+  double* x; double* r; double* p; const double* q;
+  double beta; int first; double alpha;
+  double rr;
+  double xv[CGB_U], rv[CGB_U], pv[CGB_U], qv[CGB_U];
+  __device__ void load(int64_t i, int u) {
+    xv[u] = x[i]; rv[u] = r[i]; qv[u] = q[i];
+    if (!first) pv[u] = p[i];
+  }
+  __device__ void compute(int64_t i, int u) {
+    const double pp = first ? rv[u] : rv[u] + beta * pv[u];
+    p[i] = pp;
+    x[i] = xv[u] + alpha * pp;
+    const double rn = rv[u] - alpha * qv[u];
+    r[i] = rn;
+    rr += rn * rn;
+  }
+};
+
+// Runs CG from r = b - apply(x) (stored in B.r) with rns = r.r.  Returns the
+// iteration count.  With tracking (B.c != null) *cx += alpha c.p and
+// *bax += alpha b.t follow c.x and b.(A x) through the updates.
 __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, double lam,
                            const CgBufs& B, int64_t n, int64_t m, double& rns, double delta,
-                           double floor_, int64_t max_iter, GridSync& gs, double* hp) {
+                           double floor_, int64_t max_iter, GridSync& gs, double* cx,
+                           double* bax, Prof& prof) {
   int64_t k = 0;
-  int cur = 0;
   double beta = 0.0;
-  const bool track = B.ax != nullptr;
+  const bool track = B.c != nullptr;
   while (sqrt(rns) > delta && rns > floor_ && (double)max_iter > (double)k) {
-    InVec pin;
-    if (k == 0) {
-      pin = InVec{B.pb[cur], nullptr, 0.0};
-    } else {
-      pin = InVec{B.r, B.pb[cur], beta};
-      PNew f{B.r, B.pb[cur], B.pb[cur ^ 1], beta, {}, {}};
-      stream_loop(n, f);
-      cur ^= 1;
-    }
-    const double* pc = B.pb[cur];
-    double pq[1] = {0.0};
+    const int first = k == 0;
+    const InVec pin = first ? InVec{B.r, nullptr, 0.0} : InVec{B.r, B.p, beta};
     if (recipe == CGB_RECIPE_NORMAL) {
-      EpiStore st{B.t};
-      apply_plan(F, pin, st, nullptr, gs);
-      gs.sync();
-      InVec tin{B.t, nullptr, 0.0};
-      EpiQ eq{pc, B.q, lam};
-      apply_plan(Aj, tin, eq, pq, gs);
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      {
+        EpiT et{B.t, track ? B.b : nullptr};
+        apply_plan(F, pin, et, s, gs);
+        PDots f{pin, track ? B.c : nullptr, 0.0, 0.0, {}, {}};
+        stream_loop(n, f);
+        s[1] += f.pp;
+        s[2] += f.cp;
+      }
+      gs.reduce(s);
+      prof.mark(PROF_CG_F);
+      const double alpha = rns / ((lam != 0.0 ? lam * s[1] : 0.0) + s[0]);
+      if (track) {
+        *cx += alpha * s[2];
+        *bax += alpha * s[3];
+      }
+      double rr[1] = {0.0};
+      {
+        const InVec tin{B.t, nullptr, 0.0};
+        EpiCgUpd eu{B.r, B.p, B.x, B.gx, beta, first, lam, alpha};
+        apply_plan(Aj, tin, eu, rr, gs);
+        if (B.ax) {
+          AxUpd f{B.ax, B.t, alpha, {}, {}};
+          stream_loop(m, f);
+        }
+      }
+      gs.reduce(rr);
+      prof.mark(PROF_CG_A);
+      beta = rr[0] / rns;
+      rns = rr[0];
     } else {
+      double pq[1] = {0.0};
       EpiQDirect eq{pin, B.q};
       apply_plan(F, pin, eq, pq, gs);
-    }
-    gs.reduce(pq);
-    const double alpha = rns / pq[0];
-    double red[3] = {0.0, 0.0, 0.0};
-    {
-      CgUpdateN f{B.x, B.r, pc, B.q, track ? B.gx : nullptr, B.c, alpha, 0.0, 0.0,
-                  {}, {}, {}, {}, {}, {}};
+      gs.reduce(pq);
+      prof.mark(PROF_CG_F);
+      const double alpha = rns / pq[0];
+      double rr[1] = {0.0};
+      CgUpdDirect f{B.x, B.r, B.p, B.q, beta, first, alpha, 0.0, {}, {}, {}, {}};
       stream_loop(n, f);
-      red[0] = f.rr;
-      red[2] = f.hc;
+      rr[0] = f.rr;
+      gs.reduce(rr);
+      prof.mark(PROF_CG_A);
+      beta = rr[0] / rns;
+      rns = rr[0];
     }
-    if (track) {
-      CgUpdateM f{B.ax, B.t, B.wy, B.b, alpha, 0.0, {}, {}, {}, {}};
-      stream_loop(m, f);
-      red[1] = f.hb;
-    }
-    gs.reduce(red);
-    beta = red[0] / rns;
-    rns = red[0];
-    if (hp) *hp = red[2] + red[1];
     ++k;
   }
   return k;
@@ -338,7 +418,7 @@ struct ApplyArgs {
   const double* x; double* y;
 };
 
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(ApplyArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) {
   GridSync gs(a.bar, a.partials);
   InVec in{a.x, nullptr, 0.0};
   EpiStore st{a.y};
@@ -361,7 +441,7 @@ struct DstVec {
   __device__ void operator()(int64_t i, double x) const { out[i] = x; }
 };
 
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cones(ConeArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cones(const __grid_constant__ ConeArgs a) {
   GridSync gs(a.bar, a.partials);
   SrcVec src{a.v};
   DstVec dst{a.out};
@@ -380,13 +460,14 @@ struct CgArgs {
   DevPlan F, Aj;
   int recipe; double lam;
   const double* b; double* x;
-  double* r; double* p0; double* p1; double* q; double* t;
+  double* r; double* p; double* q; double* t;
   int64_t n, m; double tol; int64_t max_iter; double eps_floor;
   double* result;  // [iterations, rns, bnorm2]
 };
 
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(CgArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) {
   GridSync gs(a.bar, a.partials);
+  Prof prof(nullptr);
   double s[2] = {0.0, 0.0};
   InVec xin{a.x, nullptr, 0.0};
   if (a.recipe == CGB_RECIPE_NORMAL) {
@@ -394,19 +475,19 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(CgArgs a) {
     apply_plan(a.F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.t, nullptr, 0.0};
-    EpiR0 e{a.b, a.x, a.r, a.p0, a.lam, 1};
+    EpiR0 e{a.b, a.x, a.r, a.lam, 1};
     apply_plan(a.Aj, tin, e, s, gs);
   } else {
-    EpiR0 e{a.b, a.x, a.r, a.p0, 0.0, 0};
+    EpiR0 e{a.b, a.x, a.r, 0.0, 0};
     apply_plan(a.F, xin, e, s, gs);
   }
   gs.reduce(s);
   double rns = s[0];
   const double delta = a.tol * sqrt(s[1]);
   const double floor_ = a.eps_floor * s[1];
-  CgBufs B{a.x, a.r, {a.p0, a.p1}, a.q, a.t, nullptr, nullptr, nullptr, nullptr, nullptr};
+  CgBufs B{a.x, a.r, a.p, a.q, a.t, nullptr, nullptr, nullptr, nullptr};
   const int64_t k = cg_loop(a.F, a.Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
-                            a.max_iter, gs, nullptr);
+                            a.max_iter, gs, nullptr, nullptr, prof);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result[0] = (double)k;
     a.result[1] = rns;
@@ -420,7 +501,7 @@ struct InnerArgs {
   const double* d1; const double* d2;
   double* z;  // n + m
   const double* c; const double* b;
-  double* r; double* p0; double* p1; double* q; double* t; double* tx;
+  double* r; double* p; double* gx; double* t; double* tx;
   int64_t n, m; double tol; int64_t max_iter; double eps_floor;
   double* result;  // [iterations, rns, rhs2, hdot]
 };
@@ -431,36 +512,37 @@ struct SideDot {  // acc += a[i] * b[i]
   __device__ void compute(int64_t, int u) { acc += xv[u] * yv[u]; }
 };
 
-// Inner block solve, exactly the reference's arithmetic (scs.py:170-187):
+// Inner block solve, the reference's arithmetic (scs.py:170-187):
 // rhs = d1 - A^T d2 ; r0 = rhs - (x0 + A^T A x0) ; CG ; z2 = d2 + A z1.
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(InnerArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) {
   GridSync gs(a.bar, a.partials);
+  Prof prof(nullptr);
   double* z1 = a.z;
   double* z2 = a.z + a.n;
-  // tx = A x0 ; then p1 (scratch) = A^T tx
+  // tx = A x0 ; then gx = A^T tx
   {
     InVec xin{z1, nullptr, 0.0};
     EpiStore st{a.tx};
     apply_plan(a.F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.tx, nullptr, 0.0};
-    EpiStore st2{a.p1};
+    EpiStore st2{a.gx};
     apply_plan(a.Aj, tin, st2, nullptr, gs);
     gs.sync();
   }
-  double s[2] = {0.0, 0.0};
+  double s[3] = {0.0, 0.0, 0.0};
   {
     InVec din{a.d2, nullptr, 0.0};
-    EpiRhs e{a.d1, z1, a.p1, a.r, a.p0};
+    EpiRhs e{a.d1, z1, a.gx, nullptr, a.r};
     apply_plan(a.Aj, din, e, s, gs);
     gs.reduce(s);
   }
   double rns = s[1];
   const double delta = a.tol * sqrt(s[0]);
   const double floor_ = a.eps_floor * s[0];
-  CgBufs B{z1, a.r, {a.p0, a.p1}, a.q, a.t, nullptr, nullptr, nullptr, nullptr, nullptr};
+  CgBufs B{z1, a.r, a.p, nullptr, a.t, nullptr, nullptr, nullptr, nullptr};
   const int64_t k = cg_loop(a.F, a.Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
-                            a.max_iter, gs, nullptr);
+                            a.max_iter, gs, nullptr, nullptr, prof);
   double h[2] = {0.0, 0.0};
   {
     InVec xin{z1, nullptr, 0.0};
@@ -495,6 +577,8 @@ struct ScsArgs {
   double denom, pr_scale, dr_scale, eps_floor;
   int64_t max_steps;
   int resid_every;
+  int stash_cap;   // doubles of shared memory per thread for the SOC stash
+  double* prof;    // PROF_N phase times (ns) or null
 };
 
 // CG tolerance exactly as the solver graph computes it (scs.py:290-311)
@@ -514,51 +598,71 @@ __device__ double cg_tolerance_graph(double k, const cgb_scs_settings& s) {
   return s.cg_base_tol + fmax(tol_capped - s.cg_base_tol, 0.0);
 }
 
-// w2 = u~ - v on the cone block: u~_y = p2 - tau_t g_y, p2 = wz2 + A p1
-// (scs.py:355, 358, 361)
-struct ScsConeSrc {
-  const double* wy; const double* ax; const double* gy; const double* vy; double tau_t;
-  __device__ double operator()(int64_t i) const {
-    return ((wy[i] + ax[i]) - tau_t * gy[i]) - vy[i];
+// Cone step of one splitting iteration on the y block (scs.py:358-366):
+//   src = u~_y - v_y with u~_y = (w_y + A p1) - tau~ g_y
+//   u_y = Pi_{K*}(src) ;  v_y <- (v_y - u~_y) + u_y  ==  u_y - src  (bitwise:
+//   fl(v - u~) = -fl(u~ - v)) ;  w_y = u_y + v_y
+// and the running sum b.w_y for the next subspace step.
+struct ConeStep {
+  const double* wy; const double* ax; const double* gy; double* vy; double* uy; double* wyo;
+  const double* b;
+  double tau;
+  int write_u;
+  __device__ __forceinline__ double src(int64_t i) const {
+    return ((wy[i] + ax[i]) - tau * gy[i]) - vy[i];
   }
-};
-// u_y <- proj ; v_y <- (v - u~) + u ; w_y <- u + v   (scs.py:365-366)
-struct ScsConeDst {
-  const double* wy_in; const double* ax; const double* gy; double* uy; double* vy; double* wy;
-  double tau_t;
-  __device__ void operator()(int64_t i, double u2) const {
-    const double ut = (wy_in[i] + ax[i]) - tau_t * gy[i];
-    const double v2 = (vy[i] - ut) + u2;
-    uy[i] = u2;
+  __device__ __forceinline__ double store(int64_t i, double s, double u2) const {
+    const double v2 = u2 - s;
+    const double w2 = u2 + v2;
+    if (write_u) uy[i] = u2;
     vy[i] = v2;
-    wy[i] = u2 + v2;
+    wyo[i] = w2;
+    return w2;
   }
 };
 
-// x block of the cone step (free): u = u~ - v, v <- (v - u~) + u, w = u + v
-struct ScsXStep {
-  const double* cgx; const double* g; double* u; double* v; double* w; double tau_t;
-  double xv[CGB_U], gv[CGB_U], vv[CGB_U];
-  __device__ void load(int64_t i, int k) { xv[k] = cgx[i]; gv[k] = g[i]; vv[k] = v[i]; }
+// elementwise segments (zero -> free in the dual, nonneg), one pass
+struct ConeElem {
+  const ConeStep* cs;
+  int64_t base;
+  int kind;
+  double bw;
+  double wv[CGB_U], av[CGB_U], gv[CGB_U], vv[CGB_U], bv[CGB_U];
+  __device__ void load(int64_t i, int u) {
+    const int64_t j = base + i;
+    wv[u] = cs->wy[j]; av[u] = cs->ax[j]; gv[u] = cs->gy[j]; vv[u] = cs->vy[j];
+    bv[u] = cs->b[j];
+  }
+  __device__ void compute(int64_t i, int u) {
+    const double s = ((wv[u] + av[u]) - cs->tau * gv[u]) - vv[u];
+    const double u2 = kind == SEG_ZERO ? s : fmax(s, 0.0);
+    bw += bv[u] * cs->store(base + i, s, u2);
+  }
+};
+
+// the free x block: v_x == 0 is an invariant of the embedding (v = (0, s,
+// kappa)), so u_x = w_x = u~_x = p1 - tau~ g_x and v_x stays 0 bitwise.
+struct XStep {
+  const double* cgx; const double* g; double* u; double* w; double tau; int write_u;
+  double xv[CGB_U], gv[CGB_U];
+  __device__ void load(int64_t i, int k) { xv[k] = cgx[i]; gv[k] = g[i]; }
   __device__ void compute(int64_t i, int k) {
-    const double ut = xv[k] - tau_t * gv[k];
-    const double u2 = ut - vv[k];
-    const double v2 = (vv[k] - ut) + u2;
-    u[i] = u2;
-    v[i] = v2;
-    w[i] = u2 + v2;
+    const double ut = xv[k] - tau * gv[k];
+    w[i] = ut;
+    if (write_u) u[i] = ut;
   }
 };
 
-struct HbSide {  // sum b.(wy + ax)
-  const double* b; const double* wy; const double* ax; double acc;
-  double bv[CGB_U], wv[CGB_U], av[CGB_U];
-  __device__ void load(int64_t i, int u) { bv[u] = b[i]; wv[u] = wy[i]; av[u] = ax[i]; }
-  __device__ void compute(int64_t, int u) { acc += bv[u] * (wv[u] + av[u]); }
-};
+// ordinal of the o-th element a thread visits in a stride-S loop -> its
+// stash slot (conflict-free: consecutive threads, consecutive words)
+__device__ __forceinline__ double* stash_slot(double* stash, int o) {
+  return stash + (size_t)o * blockDim.x + threadIdx.x;
+}
 
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(ScsArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) {
+  extern __shared__ double cgb_dyn_smem[];
   GridSync gs(a.bar, a.partials);
+  Prof prof(a.prof);
   const int64_t n = a.n, m = a.m, N = n + m + 1;
   const cgb_scs_settings& S = a.st;
   const cgb_scs_work& W = a.w;
@@ -570,50 +674,164 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(ScsArgs a) {
   const int64_t cg_max = S.cg_max_iter;
   int64_t steps = 0;
   const double* wy = W.w + n;
+  const DevCones& K = a.K;
+  const int64_t SS = gsize();
+
+  // large-SOC stash plan: slots per thread needed for every large SOC tail
+  int stash_need = 0;
+  for (int s = 0; s < K.nseg; ++s)
+    if (K.seg[s].kind == SEG_SOC_LARGE)
+      stash_need += (int)((K.seg[s].end - K.seg[s].begin - 1 + SS - 1) / SS);
+  const bool use_stash = stash_need <= a.stash_cap;
+
+  // running scalars: b.(A x) follows x through the CG updates; b.w_y is
+  // summed by every cone step for the next subspace step.
+  double bax = 0.0, bwy_part = 0.0;
+  {
+    double s[2] = {0.0, 0.0};
+    SideDot f1{a.b, W.tax, 0.0, {}, {}};
+    stream_loop(m, f1);
+    SideDot f2{a.b, wy, 0.0, {}, {}};
+    stream_loop(m, f2);
+    s[0] = f1.acc;
+    s[1] = f2.acc;
+    gs.reduce(s);
+    bax = s[0];
+    bwy_part = (blockIdx.x == 0 && threadIdx.x == 0) ? s[1] : 0.0;
+  }
+  prof.mark(PROF_INIT);
 
   while (steps < a.max_steps && (double)S.max_iters > k && !(status > 0.5)) {
     const double wtau = W.w[N - 1];
     const double vtau = W.v[N - 1];
+    const double since2 = since + 1.0;
+    const bool is_check = since2 > (double)S.check_interval - 0.5;
+    const bool last = steps + 1 >= a.max_steps || k + 1.0 >= (double)S.max_iters;
+    const bool need_resid = is_check || a.resid_every;
+    const int write_u = need_resid || last;
 
-    // -- subspace step: rhs = wz1 - A^T wz2 ; r0 = rhs - (x0 + A^T A x0)
-    //    plus h.(x0, wz2 + A x0) in case CG takes no step (scs.py:349-357)
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    // -- subspace step: rhs = w_x - A^T w_y ; r0 = rhs - (x0 + A^T A x0)
+    //    (scs.py:349-357); c.x0 and the b.w_y of the last cone step ride along
+    double s[4] = {0.0, 0.0, 0.0, bwy_part};
     {
       InVec in{wy, nullptr, 0.0};
-      EpiRhs e{W.w, W.cgx, W.gx, W.r, W.p0};
+      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r};
       apply_plan(a.Aj, in, e, s, gs);
-      HbSide fb{a.b, wy, W.tax, 0.0, {}, {}, {}};
-      stream_loop(m, fb);
-      SideDot fc{a.c, W.cgx, 0.0, {}, {}};
-      stream_loop(n, fc);
-      s[2] = fb.acc;
-      s[3] = fc.acc;
       gs.reduce(s);
     }
+    prof.mark(PROF_RHS);
     const double tol_k = cg_tolerance_graph(k, S);
     const double delta = tol_k * sqrt(s[0]);
     const double floor_ = a.eps_floor * s[0];
     double rns = s[1];
-    double hp = s[3] + s[2];
-    CgBufs B{W.cgx, W.r, {W.p0, W.p1}, W.q, W.t, W.tax, W.gx, wy, a.b, a.c};
+    double cx = s[2];
+    const double bwy = s[3];
+    CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c};
     const int64_t cgk = cg_loop(a.F, a.Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
-                                cg_max, gs, &hp);
-    const double tau_t = (wtau + hp) / a.denom;
+                                cg_max, gs, &cx, &bax, prof);
+    // tau~ = (w_tau + h.p) / (1 + h.g) with h.p = c.p1 + b.(w_y + A p1)
+    const double tau_t = (wtau + (cx + (bwy + bax))) / a.denom;
 
-    // -- cone step onto R^n x K* x R+   (scs.py:360-366)
-    ScsConeSrc src{wy, W.tax, a.g + n, W.v + n, tau_t};
-    ScsConeDst dst{wy, W.tax, a.g + n, W.u + n, W.v + n, W.w + n, tau_t};
+    // -- cone step onto R^n x K* x R+   (scs.py:358-366)
+    ConeStep cs{wy, W.tax, a.g + n, W.v + n, W.u + n, W.w + n, a.b, tau_t, write_u};
+    double bw = 0.0;
     double red[2 * CGB_MAX_LARGE_SOC];
 #pragma unroll
     for (int i = 0; i < 2 * CGB_MAX_LARGE_SOC; ++i) red[i] = 0.0;
-    if (a.K.nlarge > 0) {
-      cone_large_partials(a.K, src, red);
-      gs.reduce(red);
-    }
-    cone_project(a.K, 1, src, dst, red);
     {
-      ScsXStep f{W.cgx, a.g, W.u, W.v, W.w, tau_t, {}, {}, {}};
-      stream_loop(n, f);
+      XStep fx{W.cgx, a.g, W.u, W.w, tau_t, write_u, {}, {}};
+      stream_loop(n, fx);
+    }
+    int o_base = 0;
+    for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
+      const DevSeg sg = K.seg[sg_i];
+      if (sg.kind == SEG_SOC_LARGE) {
+        // pass A: tail sum of squares (+ stash), head from block 0
+        const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
+        double acc = 0.0;
+        int o = o_base;
+        for (int64_t i0 = gtid(); i0 < len; i0 += CGB_U * SS) {
+          double z[CGB_U];
+#pragma unroll
+          for (int u = 0; u < CGB_U; ++u) {  // clamped: all loads in flight
+            const int64_t i = i0 + u * SS;
+            z[u] = cs.src(b0 + (i < len ? i : len - 1));
+          }
+#pragma unroll
+          for (int u = 0; u < CGB_U; ++u) {
+            const int64_t i = i0 + u * SS;
+            if (i < len) {
+              acc += z[u] * z[u];
+              if (use_stash) *stash_slot(cgb_dyn_smem, o + u) = z[u];
+            }
+          }
+          o += CGB_U;
+        }
+        o_base += (int)((len + SS - 1) / SS);
+        red[sg.slot] += acc;
+        if (blockIdx.x == 0 && threadIdx.x == 0) red[K.nlarge + sg.slot] += cs.src(sg.begin);
+      } else {
+        ConeElem f{&cs, sg.begin, sg.kind, 0.0, {}, {}, {}, {}, {}};
+        stream_loop(sg.end - sg.begin, f);
+        bw += f.bw;
+      }
+    }
+    // small SOC blocks: one warp per cone, norm then projection
+    {
+      const int lane = threadIdx.x & 31;
+      const int64_t gw = (int64_t)blockIdx.x + (int64_t)gridDim.x * (threadIdx.x >> 5);
+      const int64_t nw = (int64_t)gridDim.x * CGB_WARPS;
+      for (int64_t cc = gw; cc < K.nsmall; cc += nw) {
+        const int64_t off = K.small_off[cc];
+        const int dim = K.small_dim[cc];
+        const double t = cs.src(off);
+        double nu2 = 0.0;
+        for (int i = 1 + lane; i < dim; i += 32) {
+          const double z = cs.src(off + i);
+          nu2 += z * z;
+        }
+        nu2 = warp_sum(nu2);
+        const SocCoef sc(t, sqrt(nu2));
+        __syncwarp();
+        for (int i = lane; i < dim; i += 32) {
+          const double z = cs.src(off + i);
+          bw += a.b[off + i] * cs.store(off + i, z, i == 0 ? sc.head(t) : sc.tail(z));
+        }
+      }
+    }
+    if (K.nlarge > 0) {
+      gs.reduce(red);
+      prof.mark(PROF_CONE_A);
+      // pass B: project the large SOC blocks
+      o_base = 0;
+      for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
+        const DevSeg sg = K.seg[sg_i];
+        if (sg.kind != SEG_SOC_LARGE) continue;
+        const double t = red[K.nlarge + sg.slot];
+        const SocCoef sc(t, sqrt(red[sg.slot]));
+        const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
+        int o = o_base;
+        for (int64_t i0 = gtid(); i0 < len; i0 += CGB_U * SS) {
+          double z[CGB_U], bb[CGB_U];
+#pragma unroll
+          for (int u = 0; u < CGB_U; ++u) {
+            const int64_t i = i0 + u * SS;
+            const int64_t ic = b0 + (i < len ? i : len - 1);
+            z[u] = use_stash ? (i < len ? *stash_slot(cgb_dyn_smem, o + u) : 0.0)
+                           : cs.src(ic);
+            bb[u] = a.b[ic];
+          }
+#pragma unroll
+          for (int u = 0; u < CGB_U; ++u) {
+            const int64_t i = i0 + u * SS;
+            if (i < len) bw += bb[u] * cs.store(b0 + i, z[u], sc.tail(z[u]));
+          }
+          o += CGB_U;
+        }
+        o_base += (int)((len + SS - 1) / SS);
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+          bw += a.b[sg.begin] * cs.store(sg.begin, t, sc.head(t));
+      }
     }
     const double utau = fmax(tau_t - vtau, 0.0);
     const double kappa = (vtau - tau_t) + utau;
@@ -622,15 +840,15 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(ScsArgs a) {
       W.v[N - 1] = kappa;
       W.w[N - 1] = utau + kappa;
     }
+    bwy_part = bw;
     gs.sync();
+    prof.mark(PROF_CONE_B);
 
     k += 1.0;
-    const double since2 = since + 1.0;
-    const bool is_check = since2 > (double)S.check_interval - 0.5;
     cgt += (double)cgk;
     lastcg = (double)cgk;
 
-    if (is_check || a.resid_every) {
+    if (need_resid) {
       // -- termination measures (scs.py:369-402)
       double q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       InVec uxin{W.u, nullptr, 0.0};
@@ -645,6 +863,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(ScsArgs a) {
       q[4] = fc.acc;
       q[5] = fb.acc;
       gs.reduce(q);
+      prof.mark(PROF_CHECK);
       const double eps = S.eps;
       const double pos = utau > 0.0 ? 1.0 : 0.0;
       const double tinv = pos / (utau + (1.0 - pos));
@@ -693,7 +912,7 @@ struct BarArgs {
 };
 
 // diagnostics: cost of the grid barrier / grid reduction
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(BarArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_constant__ BarArgs a) {
   GridSync gs(a.bar, a.partials);
   double acc = 0.0;
   for (int64_t i = 0; i < a.iters; ++i) {
@@ -739,6 +958,7 @@ struct cgb_ctx {
   double* partials;  // 2 banks * CGB_MAXP * max_grid
   double* result;    // small device result buffer
   double* host_result;
+  double* prof;      // k_scs phase accumulator (device, PROF_N doubles) or null
 };
 
 struct PlanStore {
@@ -757,6 +977,7 @@ struct cgb_cones {
   DevCones dc{};
   void* blob = nullptr;
   int64_t m = 0;
+  std::vector<DevSeg> segs;  // host copy (stash sizing)
 };
 
 namespace {
@@ -1147,6 +1368,7 @@ int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, in
   cgb_cones* K = new cgb_cones();
   K->blob = dev;
   K->m = off;
+  K->segs = segs;
   DevCones& C = K->dc;
   C.seg = (const DevSeg*)(dev + o_seg);
   C.small_off = (const int64_t*)(dev + o_so);
@@ -1185,9 +1407,9 @@ int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const d
   if (recipe == CGB_RECIPE_DIRECT && n != m) return fail(CGB_EINVAL, "direct CG needs square A");
   cudaStream_t s = (cudaStream_t)stream;
   double* scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * (4 * n + m + 1), s));
+  CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * (3 * n + m + 1), s));
   CgArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, recipe, lam, b, x,
-           scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, scratch + 4 * n,
+           scratch, scratch + n, scratch + 2 * n, scratch + 3 * n,
            n, m, tol, max_iter, eps_floor_for(n), ctx->result};
   int rc = launch_coop(ctx, k_cg, a, std::max(plan_smem(a.F), plan_smem(a.Aj)), s);
   if (rc == CGB_OK) {
@@ -1212,8 +1434,8 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
   const int64_t n = op->fwd.in_len, m = op->fwd.out_len;
   cudaStream_t s = (cudaStream_t)stream;
   InnerArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, d1, d2, z, c, b,
-              scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, scratch + 4 * n,
-              scratch + 4 * n + m, n, m, tol, max_iter, eps_floor_for(n), ctx->result};
+              scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, scratch + 3 * n + m,
+              n, m, tol, max_iter, eps_floor_for(n), ctx->result};
   int rc = launch_coop(ctx, k_inner, a, std::max(plan_smem(a.F), plan_smem(a.Aj)), s);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 4 * sizeof(double),
@@ -1263,8 +1485,25 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.eps_floor = eps_floor_for(prob->n);
   a.max_steps = max_steps;
   a.resid_every = resid_every_iter;
-  return launch_coop(ctx, k_scs, a, std::max(plan_smem(a.F), plan_smem(a.Aj)),
-                     (cudaStream_t)stream);
+  a.prof = ctx->prof;
+  // shared memory: conv staging of the plans, or the large-SOC stash of the
+  // cone step (one CTA per SM assumed; the kernel re-checks with the real grid)
+  const size_t plan_bytes = std::max(plan_smem(a.F), plan_smem(a.Aj));
+  const int64_t S = (int64_t)ctx->num_sms * CGB_BLOCK;
+  int64_t need = 0;
+  for (const DevSeg& sg : prob->K->segs)
+    if (sg.kind == SEG_SOC_LARGE) need += (sg.end - sg.begin - 1 + S - 1) / S;
+  const size_t stash_bytes = (size_t)need * CGB_BLOCK * sizeof(double);
+  const size_t kMaxSmem = 200 * 1024;
+  const size_t smem = std::max(plan_bytes, std::min(stash_bytes, kMaxSmem));
+  a.stash_cap = (int)(smem / (sizeof(double) * CGB_BLOCK));
+  return launch_coop(ctx, k_scs, a, smem, (cudaStream_t)stream);
+}
+
+int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc) {
+  if (!ctx) return fail(CGB_EINVAL, "null argument");
+  ctx->prof = dev_acc;
+  return CGB_OK;
 }
 
 }  // extern "C"

@@ -184,19 +184,29 @@ __device__ __forceinline__ int64_t gsize() { return (int64_t)gridDim.x * blockDi
 // Batched grid-stride loop: each thread handles CGB_U elements per step
 // (indices i, i+S, i+2S, ...), calling f.load(i, slot) for all of them
 // before f.compute(i, slot), so the loads of a batch are in flight together.
+// The ragged last batch loads from a clamped (valid) index instead of
+// branching around the loads, which would serialise them; f.load must
+// therefore be side-effect free.
 template <class F>
 __device__ __forceinline__ void stream_loop(int64_t n, F& f) {
   const int64_t S = gsize();
   for (int64_t base = gtid(); base < n; base += CGB_U * S) {
+    if (base + (CGB_U - 1) * S < n) {
 #pragma unroll
-    for (int u = 0; u < CGB_U; ++u) {
-      const int64_t i = base + u * S;
-      if (i < n) f.load(i, u);
-    }
+      for (int u = 0; u < CGB_U; ++u) f.load(base + u * S, u);
 #pragma unroll
-    for (int u = 0; u < CGB_U; ++u) {
-      const int64_t i = base + u * S;
-      if (i < n) f.compute(i, u);
+      for (int u = 0; u < CGB_U; ++u) f.compute(base + u * S, u);
+    } else {
+#pragma unroll
+      for (int u = 0; u < CGB_U; ++u) {
+        const int64_t i = base + u * S;
+        f.load(i < n ? i : n - 1, u);
+      }
+#pragma unroll
+      for (int u = 0; u < CGB_U; ++u) {
+        const int64_t i = base + u * S;
+        if (i < n) f.compute(i, u);
+      }
     }
   }
 }
@@ -297,10 +307,12 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
         for (int i0 = 0; i0 < span; i0 += 32 * CGB_U) {
           double xv[CGB_U];
 #pragma unroll
-          for (int u = 0; u < CGB_U; ++u) {
+          for (int u = 0; u < CGB_U; ++u) {  // clamped loads: no branches
             const int i = i0 + lane + 32 * u;
             const int64_t xi = xlo + i;
-            xv[u] = (i < span && xi >= 0 && xi < L.cols) ? in(xi) : 0.0;
+            const int64_t xc = xi < 0 ? 0 : (xi >= L.cols ? L.cols - 1 : xi);
+            const double v = in(xc);
+            xv[u] = (i < span && xi >= 0 && xi < L.cols) ? v : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < CGB_U; ++u) {
@@ -388,7 +400,7 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
 // Execute one level of a plan with temporary set `ts`.  Tiles are dealt
 // round-robin across blocks first (tile t -> block t mod G) so every SM
 // streams a similar share.  The epilogue gets a lane's whole tile at once:
-// epi.tile(first_row, R, left, acc, part) with rows first_row + 32 r,
+// epi.tile(first_row, tile_row0, R, left, acc, part) with rows first_row + 32 r,
 // valid while 32 r < left (see CGB_EPI_VALID) -- so it can issue all its
 // loads before its stores.
 template <class Epi>
@@ -426,7 +438,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xs, os);
     }
     if (rb.out_buf == 0) {
-      epi.tile(row0 + lane, R, nvalid - lane, acc, part);
+      epi.tile(row0 + lane, row0, R, nvalid - lane, acc, part);
     } else {
       double* dst = temp + P.temp_off[rb.out_buf - 1] + row0 + lane;
 #pragma unroll
@@ -464,6 +476,10 @@ __device__ void apply_two(const DevPlan& P1, const InVec& in1, E1& e1, const Dev
 
 // Epilogue helper: slot r of a lane tile is a valid row
 #define CGB_EPI_VALID(r) ((r) < R && 32 * (r) < left)
+// a row index that is always safe to LOAD from: the slot's row when valid,
+// else the tile's first row -- loads are issued unconditionally (no branch
+// per slot), only stores and sums are guarded
+#define CGB_EPI_IDX(j, r) (CGB_EPI_VALID(r) ? (j) + 32 * (r) : jlo)
 
 // ---------------------------------------------------------------------------
 // cone projections

@@ -281,6 +281,19 @@ class SolverPlan:
         self.csettings = settings.to_c(n)
         self.reset()
 
+    def resetup(self) -> int:
+        """Re-run the one-time setup solve g = (I+Q_z)^{-1} h on device into
+        the resident g buffer (no host copy of g; one 8-byte read-back for
+        denom).  Used by bench.py to time setup + solve with inputs resident.
+        Returns the setup CG iteration count."""
+        ca = self.cached
+        z, res, hdot = _inner_solve(self.dev, ca.c_device, ca.b_device, self.settings.setup_cg_tol,
+                                    self.settings.cg_max_iter, ca.c_device, ca.b_device)
+        ca.g_device.copy_(z)
+        ca.denom = 1.0 + hdot
+        self.cprob.denom = ca.denom
+        return int(res.iterations)
+
     def reset(self) -> None:
         """u = v = (0, 0, 1), w = u + v, warm start 0 (scs.py:448-458)."""
         for t in self.buf.values():
@@ -299,6 +312,25 @@ class SolverPlan:
     def state(self) -> np.ndarray:
         return self.buf["state"].cpu().numpy()
 
+    PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_a", "cone_b", "check",
+                      "launch_setup")
+
+    def enable_profile(self, on: bool = True) -> None:
+        """Accumulate per-phase device time of later run() calls (ns)."""
+        import torch
+        if on:
+            self._prof = torch.zeros(8, dtype=torch.float64, device="cuda")
+            ptr = _lib.ptr(self._prof)
+        else:
+            self._prof = None
+            ptr = _lib.ptr(None)
+        _lib.check(_lib.load_library().cgb_scs_profile(self.dev.ctx.handle, ptr))
+
+    def profile(self) -> dict:
+        """Seconds spent per phase since enable_profile()."""
+        vals = self._prof.cpu().numpy() * 1e-9
+        return {nm: float(vals[i]) for i, nm in enumerate(self.PROFILE_PHASES)}
+
     def loop_vars(self) -> list:
         st = self.state()
         return [self.buf["u"].cpu().numpy(), self.buf["v"].cpu().numpy(),
@@ -307,15 +339,31 @@ class SolverPlan:
                 np.array([st[_lib.ST_CGT]]),
                 np.array([st[_lib.ST_PR], st[_lib.ST_DR], st[_lib.ST_GAP]])]
 
-    # algorithmic traffic model used by bench.py for the roofline
+    # algorithmic traffic model used by bench.py for the roofline (DESIGN.md
+    # "Algorithmic bytes"): every array a phase needs is read once and every
+    # array it produces is written once; operator applies count their
+    # operand reads (input vector, matrix / CSR / kernel data, temporaries)
+    # but not their raw output, which the fused epilogues consume in place.
     def bytes_model(self) -> dict:
-        n, m = self.n, self.m
-        N = n + m + 1
-        fwd, adj = self.dev.algo_bytes(False), self.dev.algo_bytes(True)
-        cg_iter = (fwd + 8 * 2 * n) + (adj + 8 * 2 * n) + 8 * 6 * n
-        outer = (2 * adj + 8 * 4 * n) + (fwd + 8 * 3 * m) + 8 * (8 * N)
-        check = fwd + adj + 8 * 4 * m + 8 * 2 * n
-        return {"per_cg_iter": cg_iter, "per_iter": outer, "per_check": check}
+        n, m, W = self.n, self.m, 8
+        fr = self.dev.algo_bytes(False) - W * m   # forward operand reads
+        ar = self.dev.algo_bytes(True) - W * n    # adjoint operand reads
+        per_iter = (ar + W * (7 * n + 3 * m)      # rhs = w_x - A^T w_y, r0, h-dots
+                    + W * 7 * m                   # cone step: 4 reads, 3 writes
+                    + W * 6 * n)                  # free block: 3 reads, 3 writes
+        per_cg = (fr + W * (2 * n + m)            # p = r + beta p fused into A p -> t
+                  + ar + W * 2 * n                # q = p + A^T t, p.q
+                  + W * (9 * n + 5 * m))          # x, r, A^T A x, A x updates + dots
+        per_check = fr + ar + W * (3 * n + 4 * m)  # A u_x, A^T u_y, c.u_x, b.u_y
+        return {"per_iter": per_iter, "per_cg_iter": per_cg, "per_check": per_check}
+
+    def launch_bytes(self, iterations: int, cg_total: int) -> int:
+        """Algorithmic bytes of one k_scs launch that ran ``iterations``
+        splitting iterations and ``cg_total`` inner CG iterations from k=0."""
+        bm = self.bytes_model()
+        checks = iterations // max(1, self.settings.check_interval)
+        return (iterations * bm["per_iter"] + cg_total * bm["per_cg_iter"]
+                + checks * bm["per_check"])
 
 
 def build_scs_graph(problem: ConeProblem, settings: ScsSettings | None = None) -> SolverPlan:
