@@ -211,9 +211,12 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
                     double* scratch, cgb_cg_result* res, double* hdot, void* stream);
 
 /* Phase profiler: when dev_acc != NULL, later cgb_scs_run calls on this ctx
- * add the nanoseconds spent in each phase to dev_acc[0..7] (device
- * memory): 0 subspace rhs, 1 CG t = A p, 2 CG A^T t + updates, 3 cone pass
- * A, 4 cone pass B, 5 residual check, 6 per-launch setup.  NULL disables. */
+ * add the nanoseconds spent in each phase to dev_acc[0..15] (device
+ * memory): 0 subspace rhs, 1 CG t = A p, 2 CG A^T t + updates, 3 cone
+ * step x block, 4 cone step elementwise / small SOC, 5 large-SOC pass A,
+ * 6 large-SOC pass B, 7 residual check, 8 per-launch setup.  Profiling adds
+ * two grid barriers per iteration to separate the cone sub-phases.  NULL
+ * disables. */
 int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc);
 
 /* ---- diagnostics ------------------------------------------------------------ */

@@ -101,21 +101,28 @@ struct EpiR0 {
   }
 };
 
-// CG phase A (direct recipe): q = A p ; sum p.q, p from the fused accessor
+// CG phase F (direct recipe): q = A p = A r + beta q_old ; sum p.q with
+// p = r + beta p_old read pointwise
 struct EpiQDirect {
   InVec pin;
   double* qv;
+  double beta;
+  int first;
   __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
-    double pp[CGB_RC];
+    double pp[CGB_RC], qo[CGB_RC];
 #pragma unroll
-    for (int q = 0; q < CGB_RC; ++q)
-      pp[q] = pin(CGB_EPI_IDX(j, q));
+    for (int q = 0; q < CGB_RC; ++q) {
+      const int64_t jq = CGB_EPI_IDX(j, q);
+      pp[q] = pin(jq);
+      if (!first) qo[q] = qv[jq];
+    }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
-        qv[j + 32 * q] = y[q];
-        part[0] += pp[q] * y[q];
+        const double qq = first ? y[q] : y[q] + beta * qo[q];
+        qv[j + 32 * q] = qq;
+        part[0] += pp[q] * qq;
       }
     }
   }
@@ -199,11 +206,15 @@ enum ProfPhase : int {
   PROF_RHS = 0,     // subspace rhs: A^T w_y + r0 + reduce
   PROF_CG_F = 1,    // CG: t = A p + reduce
   PROF_CG_A = 2,    // CG: A^T t + fused updates + reduce
-  PROF_CONE_A = 3,  // cone pass A (+ large-SOC reduce)
-  PROF_CONE_B = 4,  // cone pass B + barrier
-  PROF_CHECK = 5,   // residual check
-  PROF_INIT = 6,    // per-launch setup (b.Ax, b.w_y)
-  PROF_N = 8
+  PROF_CONE_X = 3,  // cone step: free x block   (profiling adds a barrier)
+  PROF_CONE_E = 4,  // cone step: elementwise + small SOC segments (+ barrier)
+  PROF_CONE_A = 5,  // cone step: large-SOC pass A + reduce
+  PROF_CONE_B = 6,  // cone step: large-SOC pass B + barrier
+  PROF_CHECK = 7,   // residual check
+  PROF_INIT = 8,    // per-launch setup (b.Ax, b.w_y)
+  PROF_CONE_AR = 9, // large-SOC pass A reduce alone (profiling only)
+  PROF_CONE_AR2 = 10, // a second, warm reduction of the same size (profiling only)
+  PROF_N = 16
 };
 
 struct Prof {
@@ -226,15 +237,17 @@ struct Prof {
 // ===========================================================================
 // Two grid reductions per iteration.
 // Normal recipe, solve (lam I + A^T A) x = b:
-//   phase F : t = A p, p = r + beta p_old read through the fused accessor;
-//             sums t.t and p.p (+ c.p, b.t when tracking), then
+//   phase F : t = A p by linearity: t <- A r + beta t_old (A applied to
+//             the plain vector r, so its windows can be TMA-staged); a
+//             stream pass sums p.p (+ c.p) with p = r + beta p_old, the
+//             epilogue t.t (+ b.t), then
 //             alpha = rns / (lam p.p + t.t)       [= rns / p.(lam p + A^T A p)]
 //   phase A : y = A^T t; per element p = r + beta p_old (stored in place),
 //             q = lam p + y, x += alpha p, r -= alpha q, gx += alpha y;
 //             sum r.r ; ax += alpha t when tracking
-// Direct recipe (A square SPD): phase F q = A p, sum p.q; phase U the
-// stream update.  Same updates as the reference listing, reassociated
-// only in how p.Ap is summed.
+// Direct recipe (A square SPD): phase F q = A r + beta q_old, sum p.q;
+// phase U the stream update.  Same updates as the reference listing,
+// reassociated only in how A p and p.Ap are summed.
 struct CgBufs {
   double* x;
   double* r;
@@ -247,44 +260,68 @@ struct CgBufs {
   const double* c;  // n, tracking dots (or null)
 };
 
-// phase F (normal): t = A p ; sums t.t (slot 0), b.t (slot 3)
+// phase F (normal): t = A p by linearity, A p = A r + beta A p_old, i.e.
+// t <- A r + beta t_old ; sums t.t (slot 0), b.t (slot 3)
 struct EpiT {
   double* t;
   const double* b;
+  double beta;
+  int first;
   __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
-    double bb[CGB_RC];
-    if (b) {
+    double bb[CGB_RC], to[CGB_RC];
 #pragma unroll
-      for (int q = 0; q < CGB_RC; ++q)
-        bb[q] = b[CGB_EPI_IDX(i, q)];
+    for (int q = 0; q < CGB_RC; ++q) {
+      const int64_t iq = CGB_EPI_IDX(i, q);
+      if (b) bb[q] = b[iq];
+      if (!first) to[q] = t[iq];
     }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       if (CGB_EPI_VALID(q)) {
-        t[i + 32 * q] = y[q];
-        part[0] += y[q] * y[q];
-        if (b) part[3] += bb[q] * y[q];
+        const double tv = first ? y[q] : y[q] + beta * to[q];
+        t[i + 32 * q] = tv;
+        part[0] += tv * tv;
+        if (b) part[3] += bb[q] * tv;
       }
     }
   }
 };
 
-// phase F stream: p = pin(i) ; sums p.p (slot 1), c.p (slot 2)
+// phase F stream: p = r + beta p_old ; sums p.p (slot 1), c.p (slot 2).
+// Inputs (bulk_stream): r, [p_old unless first], [c when tracking].
+template <bool P_OLD, bool C>
 struct PDots {
-  InVec pin;
-  const double* c;
+  double beta;
   double pp, cp;
-  double pv[CGB_U], cv[CGB_U];
-  __device__ void load(int64_t i, int u) {
-    pv[u] = pin(i);
-    if (c) cv[u] = c[i];
-  }
-  __device__ void compute(int64_t, int u) {
-    pp += pv[u] * pv[u];
-    if (c) cp += cv[u] * pv[u];
+  template <int NIN>
+  __device__ __forceinline__ void compute(int64_t, const double (&v)[NIN], int64_t) {
+    const double p = P_OLD ? v[0] + beta * v[1] : v[0];
+    pp += p * p;
+    if (C) cp += v[NIN - 1] * p;
   }
 };
+
+template <bool P_OLD, bool C>
+__device__ __forceinline__ void pdots(int64_t n, const double* r, const double* p,
+                                      const double* c, double beta, double& pp, double& cp) {
+  PDots<P_OLD, C> f{beta, 0.0, 0.0};
+  if (P_OLD && C) {
+    const double* src[3] = {r, p, c};
+    bulk_stream<3>(n, src, f);
+  } else if (P_OLD) {
+    const double* src[2] = {r, p};
+    bulk_stream<2>(n, src, f);
+  } else if (C) {
+    const double* src[2] = {r, c};
+    bulk_stream<2>(n, src, f);
+  } else {
+    const double* src[1] = {r};
+    bulk_stream<1>(n, src, f);
+  }
+  pp = f.pp;
+  cp = f.cp;
+}
 
 // phase A (normal): the whole CG update in the A^T t epilogue ; sum r.r
 struct EpiCgUpd {
@@ -317,28 +354,25 @@ struct EpiCgUpd {
   }
 };
 
-struct AxUpd {  // ax += alpha t
-  double* ax; const double* t; double alpha;
-  double av[CGB_U], tv[CGB_U];
-  __device__ void load(int64_t i, int u) { av[u] = ax[i]; tv[u] = t[i]; }
-  __device__ void compute(int64_t i, int u) { ax[i] = av[u] + alpha * tv[u]; }
+struct AxUpd {  // ax += alpha t   (inputs: ax, t)
+  double* ax; double alpha;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[2], int64_t) {
+    ax[i] = v[0] + alpha * v[1];
+  }
 };
 
 // direct recipe phase U: p = r + beta p ; x += alpha p ; r -= alpha q ; sum r.r
+// (inputs: x, r, q, [p_old unless first])
 struct CgUpdDirect {
-  double* x; double* r; double* p; const double* q;
-  double beta; int first; double alpha;
+  double* x; double* r; double* p;
+  double beta; double alpha;
   double rr;
-  double xv[CGB_U], rv[CGB_U], pv[CGB_U], qv[CGB_U];
-  __device__ void load(int64_t i, int u) {
-    xv[u] = x[i]; rv[u] = r[i]; qv[u] = q[i];
-    if (!first) pv[u] = p[i];
-  }
-  __device__ void compute(int64_t i, int u) {
-    const double pp = first ? rv[u] : rv[u] + beta * pv[u];
+  template <int NIN>
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[NIN], int64_t) {
+    const double pp = NIN == 4 ? v[1] + beta * v[NIN - 1] : v[1];
     p[i] = pp;
-    x[i] = xv[u] + alpha * pp;
-    const double rn = rv[u] - alpha * qv[u];
+    x[i] = v[0] + alpha * pp;
+    const double rn = v[1] - alpha * v[2];
     r[i] = rn;
     rr += rn * rn;
   }
@@ -356,16 +390,23 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
   const bool track = B.c != nullptr;
   while (sqrt(rns) > delta && rns > floor_ && (double)max_iter > (double)k) {
     const int first = k == 0;
-    const InVec pin = first ? InVec{B.r, nullptr, 0.0} : InVec{B.r, B.p, beta};
+    const InVec rin{B.r, nullptr, 0.0};
+    const InVec pin = first ? rin : InVec{B.r, B.p, beta};
     if (recipe == CGB_RECIPE_NORMAL) {
       double s[4] = {0.0, 0.0, 0.0, 0.0};
       {
-        EpiT et{B.t, track ? B.b : nullptr};
-        apply_plan(F, pin, et, s, gs);
-        PDots f{pin, track ? B.c : nullptr, 0.0, 0.0, {}, {}};
-        stream_loop(n, f);
-        s[1] += f.pp;
-        s[2] += f.cp;
+        EpiT et{B.t, track ? B.b : nullptr, beta, first};
+        apply_plan(F, rin, et, s, gs);
+        double pp = 0.0, cp = 0.0;
+        if (first) {
+          if (track) pdots<false, true>(n, B.r, B.p, B.c, beta, pp, cp);
+          else pdots<false, false>(n, B.r, B.p, B.c, beta, pp, cp);
+        } else {
+          if (track) pdots<true, true>(n, B.r, B.p, B.c, beta, pp, cp);
+          else pdots<true, false>(n, B.r, B.p, B.c, beta, pp, cp);
+        }
+        s[1] += pp;
+        s[2] += cp;
       }
       gs.reduce(s);
       prof.mark(PROF_CG_F);
@@ -380,8 +421,9 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
         EpiCgUpd eu{B.r, B.p, B.x, B.gx, beta, first, lam, alpha};
         apply_plan(Aj, tin, eu, rr, gs);
         if (B.ax) {
-          AxUpd f{B.ax, B.t, alpha, {}, {}};
-          stream_loop(m, f);
+          AxUpd f{B.ax, alpha};
+          const double* src[2] = {B.ax, B.t};
+          bulk_stream<2>(m, src, f);
         }
       }
       gs.reduce(rr);
@@ -390,14 +432,20 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
       rns = rr[0];
     } else {
       double pq[1] = {0.0};
-      EpiQDirect eq{pin, B.q};
-      apply_plan(F, pin, eq, pq, gs);
+      EpiQDirect eq{pin, B.q, beta, first};
+      apply_plan(F, rin, eq, pq, gs);
       gs.reduce(pq);
       prof.mark(PROF_CG_F);
       const double alpha = rns / pq[0];
       double rr[1] = {0.0};
-      CgUpdDirect f{B.x, B.r, B.p, B.q, beta, first, alpha, 0.0, {}, {}, {}, {}};
-      stream_loop(n, f);
+      CgUpdDirect f{B.x, B.r, B.p, beta, alpha, 0.0};
+      if (first) {
+        const double* src[3] = {B.x, B.r, B.q};
+        bulk_stream<3>(n, src, f);
+      } else {
+        const double* src[4] = {B.x, B.r, B.q, B.p};
+        bulk_stream<4>(n, src, f);
+      }
       rr[0] = f.rr;
       gs.reduce(rr);
       prof.mark(PROF_CG_A);
@@ -419,10 +467,12 @@ struct ApplyArgs {
 };
 
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) {
+  tma_init();
+  const DevPlan& P = *cache_plan(0, a.P);
   GridSync gs(a.bar, a.partials);
   InVec in{a.x, nullptr, 0.0};
   EpiStore st{a.y};
-  apply_plan(a.P, in, st, nullptr, gs);
+  apply_plan(P, in, st, nullptr, gs);
 }
 
 struct ConeArgs {
@@ -466,27 +516,30 @@ struct CgArgs {
 };
 
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) {
+  tma_init();
+  const DevPlan& F = *cache_plan(0, a.F);
+  const DevPlan& Aj = *cache_plan(1, a.Aj);
   GridSync gs(a.bar, a.partials);
   Prof prof(nullptr);
   double s[2] = {0.0, 0.0};
   InVec xin{a.x, nullptr, 0.0};
   if (a.recipe == CGB_RECIPE_NORMAL) {
     EpiStore st{a.t};
-    apply_plan(a.F, xin, st, nullptr, gs);
+    apply_plan(F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.t, nullptr, 0.0};
     EpiR0 e{a.b, a.x, a.r, a.lam, 1};
-    apply_plan(a.Aj, tin, e, s, gs);
+    apply_plan(Aj, tin, e, s, gs);
   } else {
     EpiR0 e{a.b, a.x, a.r, 0.0, 0};
-    apply_plan(a.F, xin, e, s, gs);
+    apply_plan(F, xin, e, s, gs);
   }
   gs.reduce(s);
   double rns = s[0];
   const double delta = a.tol * sqrt(s[1]);
   const double floor_ = a.eps_floor * s[1];
   CgBufs B{a.x, a.r, a.p, a.q, a.t, nullptr, nullptr, nullptr, nullptr};
-  const int64_t k = cg_loop(a.F, a.Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
+  const int64_t k = cg_loop(F, Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result[0] = (double)k;
@@ -506,15 +559,26 @@ struct InnerArgs {
   double* result;  // [iterations, rns, rhs2, hdot]
 };
 
-struct SideDot {  // acc += a[i] * b[i]
-  const double* x; const double* y; double acc; double xv[CGB_U], yv[CGB_U];
-  __device__ void load(int64_t i, int u) { xv[u] = x[i]; yv[u] = y[i]; }
-  __device__ void compute(int64_t, int u) { acc += xv[u] * yv[u]; }
+struct SideDot {  // acc += x[i] * y[i]   (inputs: x, y)
+  double acc;
+  __device__ __forceinline__ void compute(int64_t, const double (&v)[2], int64_t) {
+    acc += v[0] * v[1];
+  }
 };
+
+__device__ __forceinline__ double side_dot(int64_t n, const double* x, const double* y) {
+  SideDot f{0.0};
+  const double* src[2] = {x, y};
+  bulk_stream<2>(n, src, f);
+  return f.acc;
+}
 
 // Inner block solve, the reference's arithmetic (scs.py:170-187):
 // rhs = d1 - A^T d2 ; r0 = rhs - (x0 + A^T A x0) ; CG ; z2 = d2 + A z1.
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) {
+  tma_init();
+  const DevPlan& F = *cache_plan(0, a.F);
+  const DevPlan& Aj = *cache_plan(1, a.Aj);
   GridSync gs(a.bar, a.partials);
   Prof prof(nullptr);
   double* z1 = a.z;
@@ -523,35 +587,33 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_cons
   {
     InVec xin{z1, nullptr, 0.0};
     EpiStore st{a.tx};
-    apply_plan(a.F, xin, st, nullptr, gs);
+    apply_plan(F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.tx, nullptr, 0.0};
     EpiStore st2{a.gx};
-    apply_plan(a.Aj, tin, st2, nullptr, gs);
+    apply_plan(Aj, tin, st2, nullptr, gs);
     gs.sync();
   }
   double s[3] = {0.0, 0.0, 0.0};
   {
     InVec din{a.d2, nullptr, 0.0};
     EpiRhs e{a.d1, z1, a.gx, nullptr, a.r};
-    apply_plan(a.Aj, din, e, s, gs);
+    apply_plan(Aj, din, e, s, gs);
     gs.reduce(s);
   }
   double rns = s[1];
   const double delta = a.tol * sqrt(s[0]);
   const double floor_ = a.eps_floor * s[0];
   CgBufs B{z1, a.r, a.p, nullptr, a.t, nullptr, nullptr, nullptr, nullptr};
-  const int64_t k = cg_loop(a.F, a.Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
+  const int64_t k = cg_loop(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   double h[2] = {0.0, 0.0};
   {
     InVec xin{z1, nullptr, 0.0};
     EpiZ2 e{nullptr, z2, a.d2, a.b};
-    apply_plan(a.F, xin, e, h, gs);
+    apply_plan(F, xin, e, h, gs);
     if (a.c) {
-      SideDot f{a.c, z1, 0.0, {}, {}};
-      stream_loop(a.n, f);
-      h[1] = f.acc;
+      h[1] = side_dot(a.n, a.c, z1);
     }
     gs.reduce(h);
   }
@@ -577,7 +639,7 @@ struct ScsArgs {
   double denom, pr_scale, dr_scale, eps_floor;
   int64_t max_steps;
   int resid_every;
-  int stash_cap;   // doubles of shared memory per thread for the SOC stash
+  int stash_cap;   // doubles of shared memory per CTA for the SOC stash
   double* prof;    // PROF_N phase times (ns) or null
 };
 
@@ -622,47 +684,77 @@ struct ConeStep {
 };
 
 // elementwise segments (zero -> free in the dual, nonneg), one pass
+// (inputs at the segment: w_y, A p1, g_y, v_y, b)
 struct ConeElem {
   const ConeStep* cs;
   int64_t base;
   int kind;
   double bw;
-  double wv[CGB_U], av[CGB_U], gv[CGB_U], vv[CGB_U], bv[CGB_U];
-  __device__ void load(int64_t i, int u) {
-    const int64_t j = base + i;
-    wv[u] = cs->wy[j]; av[u] = cs->ax[j]; gv[u] = cs->gy[j]; vv[u] = cs->vy[j];
-    bv[u] = cs->b[j];
-  }
-  __device__ void compute(int64_t i, int u) {
-    const double s = ((wv[u] + av[u]) - cs->tau * gv[u]) - vv[u];
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[5], int64_t) {
+    const double s = ((v[0] + v[1]) - cs->tau * v[2]) - v[3];
     const double u2 = kind == SEG_ZERO ? s : fmax(s, 0.0);
-    bw += bv[u] * cs->store(base + i, s, u2);
+    bw += v[4] * cs->store(base + i, s, u2);
   }
 };
 
 // the free x block: v_x == 0 is an invariant of the embedding (v = (0, s,
 // kappa)), so u_x = w_x = u~_x = p1 - tau~ g_x and v_x stays 0 bitwise.
+// (inputs: p1, g_x)
 struct XStep {
-  const double* cgx; const double* g; double* u; double* w; double tau; int write_u;
-  double xv[CGB_U], gv[CGB_U];
-  __device__ void load(int64_t i, int k) { xv[k] = cgx[i]; gv[k] = g[i]; }
-  __device__ void compute(int64_t i, int k) {
-    const double ut = xv[k] - tau * gv[k];
+  double* u; double* w; double tau; int write_u;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[2], int64_t) {
+    const double ut = v[0] - tau * v[1];
     w[i] = ut;
     if (write_u) u[i] = ut;
   }
 };
 
-// ordinal of the o-th element a thread visits in a stride-S loop -> its
-// stash slot (conflict-free: consecutive threads, consecutive words)
-__device__ __forceinline__ double* stash_slot(double* stash, int o) {
-  return stash + (size_t)o * blockDim.x + threadIdx.x;
-}
+// large SOC, pass A: tail sum of squares; the source kept in the CTA's
+// shared-memory stash (slot = offset in the CTA's range) for pass B
+// (inputs at the tail: w_y, A p1, g_y, v_y)
+struct SocPassA {
+  double tau;
+  double* stash;  // or null
+  double acc;
+  __device__ __forceinline__ void compute(int64_t, const double (&v)[4], int64_t j) {
+    const double z = ((v[0] + v[1]) - tau * v[2]) - v[3];
+    acc += z * z;
+    if (stash) stash[j] = z;
+  }
+};
+
+// large SOC, pass B from the stash (input: b at the tail)
+struct SocPassB {
+  const ConeStep* cs;
+  int64_t base;
+  SocCoef sc;
+  const double* stash;
+  double bw;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[1], int64_t j) {
+    const double z = stash[j];
+    bw += v[0] * cs->store(base + i, z, sc.tail(z));
+  }
+};
+
+// large SOC, pass B recomputing the source (inputs: w_y, A p1, g_y, v_y, b)
+struct SocPassB2 {
+  const ConeStep* cs;
+  int64_t base;
+  SocCoef sc;
+  double bw;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[5], int64_t) {
+    const double z = ((v[0] + v[1]) - cs->tau * v[2]) - v[3];
+    bw += v[4] * cs->store(base + i, z, sc.tail(z));
+  }
+};
 
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) {
-  extern __shared__ double cgb_dyn_smem[];
+  extern __shared__ __align__(16) double cgb_dyn_smem[];
+  tma_init();
   GridSync gs(a.bar, a.partials);
   Prof prof(a.prof);
+  const DevPlan& F = *cache_plan(0, a.F);
+  const DevPlan& Aj = *cache_plan(1, a.Aj);
   const int64_t n = a.n, m = a.m, N = n + m + 1;
   const cgb_scs_settings& S = a.st;
   const cgb_scs_work& W = a.w;
@@ -675,26 +767,22 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
   int64_t steps = 0;
   const double* wy = W.w + n;
   const DevCones& K = a.K;
-  const int64_t SS = gsize();
 
-  // large-SOC stash plan: slots per thread needed for every large SOC tail
-  int stash_need = 0;
+  // large-SOC stash: the pass-A source of every large SOC tail stays in the
+  // CTA's shared memory (after the bulk-stream ring) until pass B
+  int64_t stash_need = 0;
   for (int s = 0; s < K.nseg; ++s)
-    if (K.seg[s].kind == SEG_SOC_LARGE)
-      stash_need += (int)((K.seg[s].end - K.seg[s].begin - 1 + SS - 1) / SS);
-  const bool use_stash = stash_need <= a.stash_cap;
+    if (K.seg[s].kind == SEG_SOC_LARGE) stash_need += stream_span(K.seg[s].end - K.seg[s].begin - 1);
+  const bool use_stash = stash_need <= (int64_t)a.stash_cap;
+  double* const stash_base = cgb_dyn_smem;
 
   // running scalars: b.(A x) follows x through the CG updates; b.w_y is
   // summed by every cone step for the next subspace step.
   double bax = 0.0, bwy_part = 0.0;
   {
     double s[2] = {0.0, 0.0};
-    SideDot f1{a.b, W.tax, 0.0, {}, {}};
-    stream_loop(m, f1);
-    SideDot f2{a.b, wy, 0.0, {}, {}};
-    stream_loop(m, f2);
-    s[0] = f1.acc;
-    s[1] = f2.acc;
+    s[0] = side_dot(m, a.b, W.tax);
+    s[1] = side_dot(m, a.b, wy);
     gs.reduce(s);
     bax = s[0];
     bwy_part = (blockIdx.x == 0 && threadIdx.x == 0) ? s[1] : 0.0;
@@ -716,7 +804,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     {
       InVec in{wy, nullptr, 0.0};
       EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r};
-      apply_plan(a.Aj, in, e, s, gs);
+      apply_plan(Aj, in, e, s, gs);
       gs.reduce(s);
     }
     prof.mark(PROF_RHS);
@@ -727,7 +815,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double cx = s[2];
     const double bwy = s[3];
     CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c};
-    const int64_t cgk = cg_loop(a.F, a.Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
+    const int64_t cgk = cg_loop(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
                                 cg_max, gs, &cx, &bax, prof);
     // tau~ = (w_tau + h.p) / (1 + h.g) with h.p = c.p1 + b.(w_y + A p1)
     const double tau_t = (wtau + (cx + (bwy + bax))) / a.denom;
@@ -739,42 +827,23 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
 #pragma unroll
     for (int i = 0; i < 2 * CGB_MAX_LARGE_SOC; ++i) red[i] = 0.0;
     {
-      XStep fx{W.cgx, a.g, W.u, W.w, tau_t, write_u, {}, {}};
-      stream_loop(n, fx);
+      XStep fx{W.u, W.w, tau_t, write_u};
+      const double* src[2] = {W.cgx, a.g};
+      bulk_stream<2>(n, src, fx);
     }
-    int o_base = 0;
+    if (a.prof) {  // profiling only: separate the sub-phases
+      gs.sync();
+      prof.mark(PROF_CONE_X);
+    }
+    // elementwise segments (one pass each)
     for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
       const DevSeg sg = K.seg[sg_i];
-      if (sg.kind == SEG_SOC_LARGE) {
-        // pass A: tail sum of squares (+ stash), head from block 0
-        const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
-        double acc = 0.0;
-        int o = o_base;
-        for (int64_t i0 = gtid(); i0 < len; i0 += CGB_U * SS) {
-          double z[CGB_U];
-#pragma unroll
-          for (int u = 0; u < CGB_U; ++u) {  // clamped: all loads in flight
-            const int64_t i = i0 + u * SS;
-            z[u] = cs.src(b0 + (i < len ? i : len - 1));
-          }
-#pragma unroll
-          for (int u = 0; u < CGB_U; ++u) {
-            const int64_t i = i0 + u * SS;
-            if (i < len) {
-              acc += z[u] * z[u];
-              if (use_stash) *stash_slot(cgb_dyn_smem, o + u) = z[u];
-            }
-          }
-          o += CGB_U;
-        }
-        o_base += (int)((len + SS - 1) / SS);
-        red[sg.slot] += acc;
-        if (blockIdx.x == 0 && threadIdx.x == 0) red[K.nlarge + sg.slot] += cs.src(sg.begin);
-      } else {
-        ConeElem f{&cs, sg.begin, sg.kind, 0.0, {}, {}, {}, {}, {}};
-        stream_loop(sg.end - sg.begin, f);
-        bw += f.bw;
-      }
+      if (sg.kind == SEG_SOC_LARGE) continue;
+      ConeElem f{&cs, sg.begin, sg.kind, 0.0};
+      const double* src[5] = {wy + sg.begin, W.tax + sg.begin, a.g + n + sg.begin,
+                              W.v + n + sg.begin, a.b + sg.begin};
+      bulk_stream<5>(sg.end - sg.begin, src, f);
+      bw += f.bw;
     }
     // small SOC blocks: one warp per cone, norm then projection
     {
@@ -799,36 +868,59 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
         }
       }
     }
+    if (a.prof) {
+      gs.sync();
+      prof.mark(PROF_CONE_E);
+    }
+    // large SOC blocks, pass A: tail sum of squares (+ stash), head from block 0
+    {
+      int64_t so = 0;
+      for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
+        const DevSeg sg = K.seg[sg_i];
+        if (sg.kind != SEG_SOC_LARGE) continue;
+        const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
+        SocPassA f{tau_t, use_stash ? stash_base + so : nullptr, 0.0};
+        const double* src[4] = {wy + b0, W.tax + b0, a.g + n + b0, W.v + n + b0};
+        bulk_stream<4>(len, src, f);
+        so += stream_span(len);
+        red[sg.slot] += f.acc;
+        if (blockIdx.x == 0 && threadIdx.x == 0) red[K.nlarge + sg.slot] += cs.src(sg.begin);
+      }
+    }
     if (K.nlarge > 0) {
+      if (a.prof) {
+        gs.sync();
+        prof.mark(PROF_CONE_A);
+      }
       gs.reduce(red);
-      prof.mark(PROF_CONE_A);
+      prof.mark(PROF_CONE_AR);
+      if (a.prof) {  // profiling only: the same reduction again, warm
+        double red2[2 * CGB_MAX_LARGE_SOC];
+#pragma unroll
+        for (int i = 0; i < 2 * CGB_MAX_LARGE_SOC; ++i) red2[i] = 0.0;
+        gs.reduce(red2);
+        prof.mark(PROF_CONE_AR2);
+      }
       // pass B: project the large SOC blocks
-      o_base = 0;
+      int64_t so = 0;
       for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
         const DevSeg sg = K.seg[sg_i];
         if (sg.kind != SEG_SOC_LARGE) continue;
         const double t = red[K.nlarge + sg.slot];
         const SocCoef sc(t, sqrt(red[sg.slot]));
         const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
-        int o = o_base;
-        for (int64_t i0 = gtid(); i0 < len; i0 += CGB_U * SS) {
-          double z[CGB_U], bb[CGB_U];
-#pragma unroll
-          for (int u = 0; u < CGB_U; ++u) {
-            const int64_t i = i0 + u * SS;
-            const int64_t ic = b0 + (i < len ? i : len - 1);
-            z[u] = use_stash ? (i < len ? *stash_slot(cgb_dyn_smem, o + u) : 0.0)
-                           : cs.src(ic);
-            bb[u] = a.b[ic];
-          }
-#pragma unroll
-          for (int u = 0; u < CGB_U; ++u) {
-            const int64_t i = i0 + u * SS;
-            if (i < len) bw += bb[u] * cs.store(b0 + i, z[u], sc.tail(z[u]));
-          }
-          o += CGB_U;
+        if (use_stash) {
+          SocPassB f{&cs, b0, sc, stash_base + so, 0.0};
+          const double* src[1] = {a.b + b0};
+          bulk_stream<1>(len, src, f);
+          bw += f.bw;
+        } else {
+          SocPassB2 f{&cs, b0, sc, 0.0};
+          const double* src[5] = {wy + b0, W.tax + b0, a.g + n + b0, W.v + n + b0, a.b + b0};
+          bulk_stream<5>(len, src, f);
+          bw += f.bw;
         }
-        o_base += (int)((len + SS - 1) / SS);
+        so += stream_span(len);
         if (blockIdx.x == 0 && threadIdx.x == 0)
           bw += a.b[sg.begin] * cs.store(sg.begin, t, sc.head(t));
       }
@@ -855,13 +947,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
       InVec uyin{W.u + n, nullptr, 0.0};
       EpiRawP ep{W.v + n, a.b, utau};
       EpiRawD ed{a.c, utau};
-      apply_two(a.F, uxin, ep, a.Aj, uyin, ed, q, gs);
-      SideDot fc{a.c, W.u, 0.0, {}, {}};
-      stream_loop(n, fc);
-      SideDot fb{a.b, W.u + n, 0.0, {}, {}};
-      stream_loop(m, fb);
-      q[4] = fc.acc;
-      q[5] = fb.acc;
+      apply_two(F, uxin, ep, Aj, uyin, ed, q, gs);
+      q[4] = side_dot(n, a.c, W.u);
+      q[5] = side_dot(m, a.b, W.u + n);
       gs.reduce(q);
       prof.mark(PROF_CHECK);
       const double eps = S.eps;
@@ -918,10 +1006,22 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_co
   for (int64_t i = 0; i < a.iters; ++i) {
     if (a.mode == 0) {
       gs.sync();
-    } else {
+    } else if (a.mode == 1) {
       double v[1] = {1.0};
       gs.reduce(v);
       acc += v[0];
+    } else if (a.mode == 2) {
+      double v[4] = {1.0, 2.0, 3.0, 4.0};
+      gs.reduce(v);
+      acc += v[0] + v[3];
+    } else if (a.mode == 3) {
+      double v[8] = {1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0};
+      gs.reduce(v);
+      acc += v[0] + v[7];
+    } else if (a.mode == 4) {
+      gs.sync<1>();
+    } else {
+      gs.sync<0>();
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = acc;
@@ -984,6 +1084,11 @@ namespace {
 
 size_t plan_smem(const DevPlan& P) { return sizeof(double) * CGB_WARPS * (size_t)P.smem_per_warp; }
 
+// dynamic shared memory of a solver kernel: the plans' conv staging
+size_t solver_smem(const DevPlan& F, const DevPlan& Aj) {
+  return std::max(plan_smem(F), plan_smem(Aj));
+}
+
 template <class K>
 int grid_for(const cgb_ctx* ctx, K kernel, size_t smem, int* grid) {
   CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -992,8 +1097,8 @@ int grid_for(const cgb_ctx* ctx, K kernel, size_t smem, int* grid) {
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, CGB_BLOCK, smem));
   if (per_sm < 1)
     return fail(CGB_ECOOP, "kernel cannot be resident (threads/registers/shared memory)");
-  int g = ctx->num_sms * std::min(per_sm, 2);
-  if (g > ctx->max_grid) g = ctx->max_grid;
+  // one CTA per SM: the persistent kernels size every loop to the grid
+  int g = std::min(ctx->num_sms, CGB_MAXG);
   *grid = g;
   return CGB_OK;
 }
@@ -1137,6 +1242,7 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
     return d->rowblocks[x].level > d->rowblocks[y].level;  // deepest first
   });
   std::vector<DevRowBlock> rbs(d->nrowblocks);
+  const int64_t kLongBlock = 32 * CGB_RC * 256;
   std::vector<int32_t> level_rb(nlevels + 1, 0);
   std::vector<int64_t> level_tiles(nlevels, 0);
   int64_t kmax = 0;
@@ -1155,13 +1261,28 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       D.term_begin = R.term_begin;
       D.term_end = R.term_end;
       D.rfac = 1;
+      D.conv_term = -1;
+      D.pad = 0;
+      int nconv = 0;
       for (int t = R.term_begin; t < R.term_end; ++t) {
         const cgb_leaf& LF = d->leaves[d->terms[t].leaf];
         if ((LF.kind == CGB_LEAF_CONV1D || LF.kind == CGB_LEAF_CORR1D) &&
             LF.k0 <= CGB_CONV_KMAX) {
           D.rfac = CGB_RC;
           kmax = std::max<int64_t>(kmax, LF.k0);
+          ++nconv;
+          D.conv_term = t;
         }
+      }
+      if (nconv != 1) D.conv_term = -1;  // TMA staging for a single conv term only
+      // long blocks of elementwise / sparse terms: RC rows per lane too, so a
+      // tile carries enough work to amortise its setup (dense leaves keep a
+      // warp per row and R = 1)
+      if (D.rfac == 1 && R.row_end - R.row_begin >= kLongBlock) {
+        bool dense = false;
+        for (int t = R.term_begin; t < R.term_end; ++t)
+          dense |= d->leaves[d->terms[t].leaf].kind == CGB_LEAF_DENSE;
+        if (!dense) D.rfac = CGB_RC;
       }
       const int64_t rows_per_tile = 32 * (int64_t)D.rfac;
       tiles += (R.row_end - R.row_begin + rows_per_tile - 1) / rows_per_tile;
@@ -1170,6 +1291,20 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
     level_tiles[e] = tiles;
   }
   level_rb[nlevels] = idx;
+  // correlation taps of the tiled 1-d conv leaves (reversed for conv)
+  std::vector<int32_t> leaf_taps(std::max(1, d->nleaves), -1);
+  std::vector<double> taps;
+  for (int i = 0; i < d->nleaves; ++i) {
+    const cgb_leaf& L = d->leaves[i];
+    if ((L.kind == CGB_LEAF_CONV1D || L.kind == CGB_LEAF_CORR1D) && L.k0 <= CGB_CONV_KMAX) {
+      std::vector<double> kv(L.k0);
+      CUDA_TRY(cudaMemcpy(kv.data(), L.val, sizeof(double) * L.k0, cudaMemcpyDeviceToHost));
+      const int64_t nt = (L.k0 + CGB_RC - 1) / CGB_RC * CGB_RC;
+      leaf_taps[i] = (int32_t)taps.size();
+      for (int64_t j = 0; j < nt; ++j)
+        taps.push_back(j < L.k0 ? kv[L.kind == CGB_LEAF_CONV1D ? L.k0 - 1 - j : j] : 0.0);
+    }
+  }
   Blob blob;
   size_t o_leaves = blob.add(d->leaves, sizeof(cgb_leaf) * d->nleaves);
   size_t o_terms = blob.add(d->terms, sizeof(cgb_term) * d->nterms);
@@ -1177,6 +1312,8 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   size_t o_lrb = blob.add(level_rb.data(), sizeof(int32_t) * level_rb.size());
   size_t o_lt = blob.add(level_tiles.data(), sizeof(int64_t) * level_tiles.size());
   size_t o_to = blob.add(temp_off.data(), sizeof(int64_t) * temp_off.size());
+  size_t o_lta = blob.add(leaf_taps.data(), sizeof(int32_t) * leaf_taps.size());
+  size_t o_taps = blob.add(taps.data(), sizeof(double) * taps.size());
   char* dev = nullptr;
   CUDA_TRY(cudaMalloc(&dev, blob.host.size() + 256));
   CUDA_TRY(cudaMemcpy(dev, blob.host.data(), blob.host.size(), cudaMemcpyHostToDevice));
@@ -1192,14 +1329,20 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   P.level_rb = (const int32_t*)(dev + o_lrb);
   P.level_tiles = (const int64_t*)(dev + o_lt);
   P.temp_off = (const int64_t*)(dev + o_to);
+  P.leaf_taps = (const int32_t*)(dev + o_lta);
+  P.taps = (const double*)(dev + o_taps);
+  P.meta = dev;
+  P.meta_bytes = (int32_t)std::min<size_t>(blob.host.size(), INT32_MAX);
   P.temp[0] = ps->temps;
   P.temp[1] = ps->temps ? ps->temps + temp_total : nullptr;
   P.nlevels = nlevels;
+  P.pad = 0;
   if (kmax > 0) {
-    const int64_t groups = (kmax + CGB_RC - 1) / CGB_RC;
-    P.smem_cc = (int32_t)(groups * CGB_RC + 1) & ~1;
-    P.smem_xs = (int32_t)((32 * CGB_RC + (groups + 1) * CGB_RC + 1) & ~1);
-    P.smem_per_warp = P.smem_cc + P.smem_xs + 32 * CGB_RC + 1;
+    // per warp: window buffer 0 | window buffer 1 | output transpose
+    const int64_t ntaps = (kmax + CGB_RC - 1) / CGB_RC * CGB_RC;
+    P.smem_cc = 0;
+    P.smem_xs = (int32_t)((32 * CGB_RC + ntaps + 2 + 1) & ~1);
+    P.smem_per_warp = (2 * P.smem_xs + 32 * CGB_RC + 1 + 1) & ~1;
   } else {
     P.smem_cc = 0;
     P.smem_xs = 0;
@@ -1411,7 +1554,7 @@ int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const d
   CgArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, recipe, lam, b, x,
            scratch, scratch + n, scratch + 2 * n, scratch + 3 * n,
            n, m, tol, max_iter, eps_floor_for(n), ctx->result};
-  int rc = launch_coop(ctx, k_cg, a, std::max(plan_smem(a.F), plan_smem(a.Aj)), s);
+  int rc = launch_coop(ctx, k_cg, a, solver_smem(a.F, a.Aj), s);
   if (rc == CGB_OK) {
     CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 3 * sizeof(double),
                              cudaMemcpyDeviceToHost, s));
@@ -1436,7 +1579,7 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
   InnerArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, d1, d2, z, c, b,
               scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, scratch + 3 * n + m,
               n, m, tol, max_iter, eps_floor_for(n), ctx->result};
-  int rc = launch_coop(ctx, k_inner, a, std::max(plan_smem(a.F), plan_smem(a.Aj)), s);
+  int rc = launch_coop(ctx, k_inner, a, solver_smem(a.F, a.Aj), s);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 4 * sizeof(double),
                            cudaMemcpyDeviceToHost, s));
@@ -1487,16 +1630,18 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.resid_every = resid_every_iter;
   a.prof = ctx->prof;
   // shared memory: conv staging of the plans, or the large-SOC stash of the
-  // cone step (one CTA per SM assumed; the kernel re-checks with the real grid)
-  const size_t plan_bytes = std::max(plan_smem(a.F), plan_smem(a.Aj));
-  const int64_t S = (int64_t)ctx->num_sms * CGB_BLOCK;
+  // cone step, whichever is larger (never live together; one CTA per SM --
+  // the kernel re-checks the stash need with the real grid)
+  const size_t base = solver_smem(a.F, a.Aj);
+  const int64_t S = (int64_t)std::min(ctx->num_sms, CGB_MAXG) * CGB_BLOCK;
   int64_t need = 0;
   for (const DevSeg& sg : prob->K->segs)
-    if (sg.kind == SEG_SOC_LARGE) need += (sg.end - sg.begin - 1 + S - 1) / S;
-  const size_t stash_bytes = (size_t)need * CGB_BLOCK * sizeof(double);
+    if (sg.kind == SEG_SOC_LARGE)
+      need += (sg.end - sg.begin - 1 + CGB_U * S - 1) / (CGB_U * S) * CGB_U * CGB_BLOCK;
   const size_t kMaxSmem = 200 * 1024;
-  const size_t smem = std::max(plan_bytes, std::min(stash_bytes, kMaxSmem));
-  a.stash_cap = (int)(smem / (sizeof(double) * CGB_BLOCK));
+  size_t smem = base;
+  if (sizeof(double) * (size_t)need <= kMaxSmem) smem = std::max(smem, sizeof(double) * (size_t)need);
+  a.stash_cap = (int)(smem / sizeof(double));
   return launch_coop(ctx, k_scs, a, smem, (cudaStream_t)stream);
 }
 

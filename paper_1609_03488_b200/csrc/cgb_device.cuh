@@ -16,12 +16,15 @@
 #define CGB_MINB 1
 #endif
 #define CGB_MAXP 16          // reduction slots per grid reduction
-#define CGB_MAXG 320         // largest grid the reductions are unrolled for
+#ifndef CGB_BAR_FENCE
+#define CGB_BAR_FENCE 2      // grid-barrier fence flavour (see GridSync::sync)
+#endif
+#define CGB_MAXG 160         // largest grid the reductions are unrolled for (148 SMs x 1)
 #define CGB_MAX_LARGE_SOC 4  // SOC blocks reduced across the whole grid
 #ifndef CGB_RC
 #define CGB_RC 9             // rows per lane in convolution tiles (odd: no bank conflicts)
 #endif
-#define CGB_CONV_KMAX 1024   // longest 1-d kernel staged in shared memory
+#define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
 #define CGB_U 4              // elements per thread per batch in streaming loops
 
 namespace cgb {
@@ -32,9 +35,14 @@ namespace cgb {
 struct DevRowBlock {
   int64_t row_begin, row_end, tile_begin;
   int32_t out_buf, term_begin, term_end;
-  int32_t rfac;  // rows per lane in this block's tiles (1 or CGB_RC)
+  int32_t rfac;       // rows per lane in this block's tiles (1 or CGB_RC)
+  int32_t conv_term;  // the block's only 1-d conv term (TMA-staged), or -1
+  int32_t pad;
 };
 
+// All metadata arrays of a plan live in one device blob [meta, meta +
+// meta_bytes) so a kernel can copy the whole plan into shared memory once
+// (cache_plan) and rebase the pointers.
 struct DevPlan {
   const cgb_leaf* leaves;
   const cgb_term* terms;
@@ -42,11 +50,18 @@ struct DevPlan {
   const int32_t* level_rb;     // nlevels + 1, execution order (deepest first)
   const int64_t* level_tiles;  // nlevels
   const int64_t* temp_off;     // ntemps
+  const int32_t* leaf_taps;    // per leaf: offset into taps, or -1
+  const double* taps;          // correlation taps of the tiled 1-d conv leaves
+                               // (reversed for conv), zero padded to RC
+  const char* meta;            // blob holding every array above
   double* temp[2];             // two temporary sets (two applications per phase)
+  int32_t meta_bytes;
   int32_t nlevels;
   int32_t smem_per_warp;  // doubles of dynamic shared memory per warp
-  int32_t smem_cc;        // taps part (conv kernel, zero padded)
-  int32_t smem_xs;        // staged-input part (output transpose follows)
+  int32_t smem_cc;        // (unused, 0)
+  int32_t smem_xs;        // one staged-input window; two windows, then the
+                          // 32*RC+1 output transpose
+  int32_t pad;
   int64_t in_len, out_len;
 };
 
@@ -92,6 +107,99 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, sm_90+) with mbarrier completion
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// arrive (count 1) announcing `bytes` of transaction, then the bulk copy
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .b64 st;\n"
+      " mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "CGB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra CGB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// per-warp pair of mbarriers for the double-buffered conv windows, and the
+// parity each buffer's next completion will have (bit b for buffer b)
+__shared__ uint64_t cgb_mbar[CGB_WARPS][2];
+__shared__ uint32_t cgb_mbar_phase[CGB_WARPS];
+
+// every persistent kernel calls this first (all threads)
+__device__ __forceinline__ void tma_init() {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (lane == 0) {
+    mbar_init(&cgb_mbar[wib][0], 1);
+    mbar_init(&cgb_mbar[wib][1], 1);
+    cgb_mbar_phase[wib] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// plan cache: a kernel copies its (small) plans into shared memory once, so
+// the per-tile metadata lookups of every later phase are shared loads
+// ---------------------------------------------------------------------------
+#define CGB_PLAN_SMEM 6144
+__shared__ __align__(16) char cgb_plan_meta[2][CGB_PLAN_SMEM];
+__shared__ DevPlan cgb_plan_view[2];
+
+template <class T>
+__device__ __forceinline__ const T* rebase(const T* p, const char* from, char* to) {
+  return p ? reinterpret_cast<const T*>(to + (reinterpret_cast<const char*>(p) - from)) : p;
+}
+
+// all threads; returns the shared copy, or P itself if it does not fit
+__device__ __forceinline__ const DevPlan* cache_plan(int slot, const DevPlan& P) {
+  if (P.meta_bytes > CGB_PLAN_SMEM || P.meta == nullptr) return &P;
+  const int4* src = reinterpret_cast<const int4*>(P.meta);
+  int4* dst = reinterpret_cast<int4*>(cgb_plan_meta[slot]);
+  for (int i = threadIdx.x; i < (P.meta_bytes + 15) / 16; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x == 0) {
+    DevPlan v = P;
+    char* to = cgb_plan_meta[slot];
+    v.leaves = rebase(P.leaves, P.meta, to);
+    v.terms = rebase(P.terms, P.meta, to);
+    v.rbs = rebase(P.rbs, P.meta, to);
+    v.level_rb = rebase(P.level_rb, P.meta, to);
+    v.level_tiles = rebase(P.level_tiles, P.meta, to);
+    v.temp_off = rebase(P.temp_off, P.meta, to);
+    v.leaf_taps = rebase(P.leaf_taps, P.meta, to);
+    v.taps = rebase(P.taps, P.meta, to);
+    cgb_plan_view[slot] = v;
+  }
+  __syncthreads();
+  return &cgb_plan_view[slot];
+}
+
 struct GridSync {
   GridBar* bar;
   double* partials;  // [2 banks][CGB_MAXP][grid]
@@ -101,11 +209,18 @@ struct GridSync {
   __device__ GridSync(GridBar* b, double* p) : bar(b), partials(p), bank(0), target(0) {}
 
   // All threads of all blocks must call this (uniform control flow).
+  // FENCE selects the ordering around the arrival: 2 = fence.sc before and
+  // after (cooperative-groups style), 1 = fence.acq_rel before the release
+  // arrival, 0 = release / acquire only.  The CTA barrier on either side
+  // carries the other threads' accesses (bar.sync is morally strong, and
+  // release / acquire are cumulative over what thread 0 has observed).
+  template <int FENCE = CGB_BAR_FENCE>
   __device__ void sync() {
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
-      __threadfence();
+      if (FENCE == 2) __threadfence();
+      if (FENCE == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       red_release_add(&bar->count, 1ull);
       if (ld_acquire_u64(&bar->count) < target) {
         const uint64_t t0 = globaltimer();
@@ -116,17 +231,20 @@ struct GridSync {
           }
         }
       }
-      __threadfence();
+      if (FENCE == 2) __threadfence();
     }
     __syncthreads();
   }
 
   // Sum v[0..NP) over every thread of the grid.  The result is bitwise
   // identical in every thread of every block (fixed summation order), so
-  // control decisions taken on it stay grid-uniform.
+  // control decisions taken on it stay grid-uniform.  Warp p owns slot p:
+  // it folds the block's warp sums into the block partial before the
+  // barrier and, after it, reads all gridDim.x partials of its slot with
+  // every load in flight at once (one L2 round trip for any NP <= 16).
   template <int NP>
   __device__ void reduce(double (&v)[NP]) {
-    static_assert(NP <= CGB_MAXP, "too many reduction slots");
+    static_assert(NP <= CGB_MAXP && NP <= CGB_WARPS, "too many reduction slots");
     __shared__ double red_smem[CGB_WARPS][CGB_MAXP];
     __shared__ double red_out[CGB_MAXP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -140,34 +258,28 @@ struct GridSync {
     __syncthreads();
     const int G = gridDim.x;
     double* bankp = partials + (size_t)bank * CGB_MAXP * G;
-    if (wid == 0) {
+    if (wid < NP) {
+      double s = lane < CGB_WARPS ? red_smem[lane][wid] : 0.0;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        double s = lane < CGB_WARPS ? red_smem[lane][p] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) bankp[(size_t)p * G + blockIdx.x] = s;
-      }
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) bankp[(size_t)wid * G + blockIdx.x] = s;
     }
     sync();
-    // warp 0 reads all partials (independent loads in flight) and broadcasts
-    if (wid == 0) {
+    if (wid < NP) {
       constexpr int NI = (CGB_MAXG + 31) / 32;
+      const double* src = bankp + (size_t)wid * G;
+      double x[NI];
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        double x[NI];
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-          const int idx = lane + 32 * i;
-          x[i] = idx < G ? __ldcg(bankp + (size_t)p * G + idx) : 0.0;
-        }
-        double s = 0.0;
-#pragma unroll
-        for (int i = 0; i < NI; ++i) s += x[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) red_out[p] = s;
+      for (int i = 0; i < NI; ++i) {
+        const int idx = lane + 32 * i;
+        x[i] = idx < G ? __ldcg(src + idx) : 0.0;
       }
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) s += x[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) red_out[wid] = s;
     }
     __syncthreads();
 #pragma unroll
@@ -211,6 +323,42 @@ __device__ __forceinline__ void stream_loop(int64_t n, F& f) {
   }
 }
 
+// Stream pass over [0, n) of NIN input vectors: f.compute(i, v, j) with
+// v[a] = src[a][i] and j a per-CTA slot index unique to (thread, visit)
+// -- the same in every pass over the same n, so a pass can leave values in
+// shared memory (stash) for a later one.  Grid-stride, CGB_U elements per
+// thread per batch, every load of a batch in flight before the first use
+// (the ragged batch loads clamped indices).  Contiguous per-CTA ranges fed
+// by TMA bulk copies were measured slower on B200 for these 1e6-element
+// passes (one block-wide sync per chunk), see DESIGN.md.
+template <int NIN, class F>
+__device__ __forceinline__ void bulk_stream(int64_t n, const double* const (&src)[NIN], F& f) {
+  const int64_t S = gsize();
+  int b = 0;
+  for (int64_t base = gtid(); base < n; base += CGB_U * S, ++b) {
+    const bool full = base + (CGB_U - 1) * S < n;
+    double v[CGB_U][NIN];
+#pragma unroll
+    for (int u = 0; u < CGB_U; ++u) {
+      const int64_t i = base + u * S;
+      const int64_t ic = full || i < n ? i : n - 1;
+#pragma unroll
+      for (int a = 0; a < NIN; ++a) v[u][a] = src[a][ic];
+    }
+#pragma unroll
+    for (int u = 0; u < CGB_U; ++u) {
+      const int64_t i = base + u * S;
+      if (full || i < n) f.compute(i, v[u], (int64_t)(b * CGB_U + u) * blockDim.x + threadIdx.x);
+    }
+  }
+}
+
+// doubles of per-CTA stash a bulk_stream pass over `len` elements can fill
+__device__ __forceinline__ int64_t stream_span(int64_t len) {
+  const int64_t S = gsize();
+  return (len + CGB_U * S - 1) / (CGB_U * S) * CGB_U * blockDim.x;
+}
+
 // ---------------------------------------------------------------------------
 // operator-plan executor
 // ---------------------------------------------------------------------------
@@ -236,20 +384,63 @@ __device__ __forceinline__ double warp_sum(double s) {
   return s;
 }
 
+// taps of a 1-d conv leaf as a correlation kernel (reversed for conv) are
+// prepared by the host, zero padded to a multiple of CGB_RC
+__device__ __forceinline__ int conv_ntaps(int64_t k) {
+  return (int)((k + CGB_RC - 1) / CGB_RC) * CGB_RC;
+}
+// staged window length of an R == CGB_RC tile: 32*RC outputs + taps
+__device__ __forceinline__ int conv_span(int64_t k) { return 32 * CGB_RC + conv_ntaps(k); }
+
+// Register-blocked valid correlation over a staged window: lane l computes
+// the CGB_RC consecutive outputs o0 = l*RC .. o0+RC-1,
+//   y[r] = sum_j cc[j] xs[o0 + r + j],
+// with a sliding register window -- one shared load of the window and one
+// (broadcast) tap load per RC FMAs -- then transposes the results to the
+// lane-strided tile layout through `os` and accumulates alpha * y.
+__device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const double* cc,
+                                             double* os, double (&acc)[CGB_RC], double alpha,
+                                             int nvalid, int lane) {
+  const int ngroups = (int)((k + CGB_RC - 1) / CGB_RC);
+  const int o0 = lane * CGB_RC;
+  double y[CGB_RC], w[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) {
+    y[r] = 0.0;
+    w[r] = xs[o0 + r];
+  }
+  for (int g = 0; g < ngroups; ++g) {
+    const double* xg = xs + o0 + g * CGB_RC + CGB_RC;
+    const double* cg = cc + g * CGB_RC;
+#pragma unroll
+    for (int jj = 0; jj < CGB_RC; ++jj) {
+      const double cj = cg[jj];
+#pragma unroll
+      for (int r = 0; r < CGB_RC; ++r) y[r] = fma(cj, w[(jj + r) % CGB_RC], y[r]);
+      w[jj] = xg[jj];  // slot jj slides from x[o0+gRC+jj] to x[o0+gRC+jj+RC]
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) os[o0 + r] = y[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r)
+    if (lane + 32 * r < nvalid) acc[r] += alpha * os[lane + 32 * r];
+  __syncwarp();
+}
+
 // Contribution of one leaf to a warp tile.  The tile holds 32*R rows
 // starting at leaf-local row lrow0; lane l owns rows lrow0 + l + 32 r
 // (r < R), so epilogue stores are coalesced.  acc[r] accumulates.
 // Warp-collective: every lane of the warp must call it.
 //
 // 1-d convolution / correlation leaves in R == CGB_RC tiles run the
-// register-blocked path: the warp stages its taps and its input window
-// (tile + halo, through the fused accessor) in shared memory once, each
-// lane then computes CGB_RC *consecutive* outputs with a sliding register
-// window (2*RC-1 + RC shared loads per RC*RC FMAs), and the results are
-// transposed back to the lane-strided layout through shared memory.
+// register-blocked path (conv_compute) on a window staged in shared memory:
+// by TMA in run_level for interior tiles, by hand (zero-filled edges) here.
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
-                                          double (&acc)[CGB_RC], int lane, double* cc,
+                                          double (&acc)[CGB_RC], int lane, const double* cc,
                                           double* xs, double* os) {
   switch (L.kind) {
     case CGB_LEAF_IDENTITY: {
@@ -293,17 +484,11 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
     case CGB_LEAF_CORR1D: {
       const bool conv = L.kind == CGB_LEAF_CONV1D;
       const int64_t k = L.k0;
-      if (R == CGB_RC) {
-        // staged window: xs[i] = x[xlo + i]; every output is then the valid
-        // correlation sum_j cc[j] xs[o + j] with cc = reversed kernel for conv
+      if (R == CGB_RC && cc) {
+        // edge tile (window leaves [0, cols)): stage by hand with zero fill
         const int64_t xlo = conv ? lrow0 - (k - 1) : lrow0;
-        const int ngroups = (int)((k + CGB_RC - 1) / CGB_RC);
-        const int ntaps = ngroups * CGB_RC;
-        const int span = 32 * CGB_RC + ntaps + CGB_RC;
-        const int o0 = lane * CGB_RC;
+        const int span = conv_span(k);
         __syncwarp();
-        for (int i = lane; i < ntaps; i += 32)
-          cc[i] = i < k ? __ldg(L.val + (conv ? k - 1 - i : i)) : 0.0;
         for (int i0 = 0; i0 < span; i0 += 32 * CGB_U) {
           double xv[CGB_U];
 #pragma unroll
@@ -321,27 +506,7 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
           }
         }
         __syncwarp();
-        double y[CGB_RC];
-#pragma unroll
-        for (int r = 0; r < CGB_RC; ++r) y[r] = 0.0;
-        for (int g = 0; g < ngroups; ++g) {
-          const int j0 = g * CGB_RC;
-          double w[2 * CGB_RC - 1];
-#pragma unroll
-          for (int i = 0; i < 2 * CGB_RC - 1; ++i) w[i] = xs[o0 + j0 + i];
-#pragma unroll
-          for (int jj = 0; jj < CGB_RC; ++jj) {
-            const double cj = cc[j0 + jj];
-#pragma unroll
-            for (int r = 0; r < CGB_RC; ++r) y[r] += cj * w[r + jj];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < CGB_RC; ++r) os[o0 + r] = y[r];
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < CGB_RC; ++r)
-          if (lane + 32 * r < nvalid) acc[r] += alpha * os[lane + 32 * r];
+        conv_compute(k, xs, cc, os, acc, alpha, nvalid, lane);
       } else {
 #pragma unroll
         for (int r = 0; r < CGB_RC; ++r) {
@@ -397,55 +562,155 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
   }
 }
 
+// Window of a tile's TMA-staged conv term: the bulk copy reads `bytes` from
+// the 16-byte aligned `src`; the window starts `shift` doubles into the
+// shared buffer.  ok == false: no conv term, a fused (two-vector) input, or a
+// window reaching outside the input (edge tile) -- staged by hand instead.
+struct ConvWin {
+  const double* src;
+  uint32_t bytes;
+  int shift;
+  bool ok;
+};
+
+__device__ __forceinline__ ConvWin conv_window(const DevPlan& P, const DevRowBlock& rb,
+                                               int64_t row0, const InVec& in,
+                                               const double* temp) {
+  ConvWin w{nullptr, 0u, 0, false};
+  if (rb.conv_term < 0) return w;
+  const cgb_term tm = P.terms[rb.conv_term];
+  const cgb_leaf L = P.leaves[tm.leaf];
+  const double* base;
+  if (tm.in_buf == 0) {
+    if (in.b) return w;
+    base = in.a + tm.in_off;
+  } else {
+    base = temp + P.temp_off[tm.in_buf - 1] + tm.in_off;
+  }
+  const int64_t k = L.k0;
+  const int64_t lrow0 = row0 - tm.row_origin;
+  const int64_t xlo = L.kind == CGB_LEAF_CONV1D ? lrow0 - (k - 1) : lrow0;
+  const int span = conv_span(k);
+  if (xlo < 0 || xlo + span > L.cols) return w;
+  const double* a = base + xlo;
+  w.shift = (int)((reinterpret_cast<uintptr_t>(a) >> 3) & 1);
+  w.src = a - w.shift;
+  w.bytes = (uint32_t)(((span + w.shift) * 8 + 15) & ~15);
+  w.ok = true;
+  return w;
+}
+
+__device__ __forceinline__ int find_rowblock(const DevPlan& P, int lo, int hi, int64_t tile) {
+  hi -= 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.rbs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// lane 0 issues the bulk copy of a window into `dst` (after the warp's
+// generic-proxy reads of that buffer are fenced off)
+__device__ __forceinline__ void issue_window(const ConvWin& w, double* dst, uint64_t* bar,
+                                             int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    fence_proxy_async();
+    bulk_load(dst, w.src, w.bytes, bar);
+  }
+}
+
 // Execute one level of a plan with temporary set `ts`.  Tiles are dealt
 // round-robin across blocks first (tile t -> block t mod G) so every SM
-// streams a similar share.  The epilogue gets a lane's whole tile at once:
+// streams a similar share.  A warp's conv windows are double buffered: the
+// TMA copy of its next tile's window is in flight while it computes the
+// current one.  The epilogue gets a lane's whole tile at once:
 // epi.tile(first_row, tile_row0, R, left, acc, part) with rows first_row + 32 r,
 // valid while 32 r < left (see CGB_EPI_VALID) -- so it can issue all its
 // loads before its stores.
 template <class Epi>
 __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
                           double* part) {
-  extern __shared__ double cgb_dyn_smem[];
+  extern __shared__ __align__(16) double cgb_dyn_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* cc = cgb_dyn_smem + (size_t)wib * P.smem_per_warp;
-  double* xs = cc + P.smem_cc;
-  double* os = xs + P.smem_xs;
+  double* xsb0 = cgb_dyn_smem + (size_t)wib * P.smem_per_warp;
+  double* xsb1 = xsb0 + P.smem_xs;
+  double* os = xsb1 + P.smem_xs;
+  uint64_t* bar = cgb_mbar[wib];
   const int64_t G = gridDim.x;
+  const int64_t stride = G * CGB_WARPS;
   const int64_t T = P.level_tiles[e];
   const int rb_lo = P.level_rb[e], rb_hi = P.level_rb[e + 1];
-  double* temp = P.temp[ts];
-  for (int64_t tile = blockIdx.x + G * wib; tile < T; tile += G * CGB_WARPS) {
-    int lo = rb_lo, hi = rb_hi - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (P.rbs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
-    }
-    const DevRowBlock rb = P.rbs[lo];
+  const double* temp = P.temp[ts];
+  __syncwarp();
+  uint32_t ph = cgb_mbar_phase[wib];
+  int cur = 0;
+  int64_t tile = blockIdx.x + G * wib;
+  int rbi = 0;
+  int64_t row0 = 0;
+  ConvWin win{nullptr, 0u, 0, false};
+  if (tile < T) {
+    rbi = find_rowblock(P, rb_lo, rb_hi, tile);
+    const DevRowBlock& rb = P.rbs[rbi];
+    row0 = rb.row_begin + (tile - rb.tile_begin) * (32 * rb.rfac);
+    win = conv_window(P, rb, row0, in, temp);
+    if (win.ok) issue_window(win, xsb0, &bar[0], lane);
+  }
+  for (; tile < T; tile += stride) {
+    const DevRowBlock rb = P.rbs[rbi];
     const int R = rb.rfac;
-    const int64_t row0 = rb.row_begin + (tile - rb.tile_begin) * (32 * R);
     const int64_t rem = rb.row_end - row0;
     const int nvalid = rem < 32 * R ? (int)rem : 32 * R;
+    double* xcur = cur ? xsb1 : xsb0;
+    // prefetch the next tile's window into the other buffer
+    const int64_t ntile = tile + stride;
+    int nrbi = rbi;
+    int64_t nrow0 = 0;
+    ConvWin nwin{nullptr, 0u, 0, false};
+    if (ntile < T) {
+      nrbi = find_rowblock(P, rb_lo, rb_hi, ntile);
+      const DevRowBlock& nrb = P.rbs[nrbi];
+      nrow0 = nrb.row_begin + (ntile - nrb.tile_begin) * (32 * nrb.rfac);
+      nwin = conv_window(P, nrb, nrow0, in, temp);
+      if (nwin.ok) issue_window(nwin, cur ? xsb0 : xsb1, &bar[cur ^ 1], lane);
+    }
     double acc[CGB_RC];
 #pragma unroll
     for (int r = 0; r < CGB_RC; ++r) acc[r] = 0.0;
     for (int t = rb.term_begin; t < rb.term_end; ++t) {
       const cgb_term tm = P.terms[t];
       const cgb_leaf L = P.leaves[tm.leaf];
+      const int toff = P.leaf_taps[tm.leaf];
+      const double* cc = toff >= 0 ? P.taps + toff : nullptr;
+      if (t == rb.conv_term && win.ok) {
+        // the window was issued one tile ago; wait for its bytes
+        mbar_wait(&bar[cur], (ph >> cur) & 1u);
+        ph ^= 1u << cur;
+        __syncwarp();
+        conv_compute(L.k0, xcur + win.shift, cc, os, acc, tm.alpha, nvalid, lane);
+        continue;
+      }
       const InVec tin = tm.in_buf == 0
                             ? in.shift(tm.in_off)
                             : InVec{temp + P.temp_off[tm.in_buf - 1] + tm.in_off, nullptr, 0.0};
-      leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xs, os);
+      leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os);
     }
     if (rb.out_buf == 0) {
       epi.tile(row0 + lane, row0, R, nvalid - lane, acc, part);
     } else {
-      double* dst = temp + P.temp_off[rb.out_buf - 1] + row0 + lane;
+      double* dst = P.temp[ts] + P.temp_off[rb.out_buf - 1] + row0 + lane;
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r)
         if (r < R && lane + 32 * r < nvalid) dst[32 * r] = acc[r];
     }
+    cur ^= 1;
+    rbi = nrbi;
+    row0 = nrow0;
+    win = nwin;
   }
+  __syncwarp();
+  if (lane == 0) cgb_mbar_phase[wib] = ph;
+  __syncwarp();
 }
 
 // Full application; levels separated by grid barriers.  No barrier after the

@@ -312,14 +312,14 @@ class SolverPlan:
     def state(self) -> np.ndarray:
         return self.buf["state"].cpu().numpy()
 
-    PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_a", "cone_b", "check",
-                      "launch_setup")
+    PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_x", "cone_elem",
+                      "cone_soc_a", "cone_soc_b", "check", "launch_setup", "cone_soc_a_reduce", "reduce8_warm")
 
     def enable_profile(self, on: bool = True) -> None:
         """Accumulate per-phase device time of later run() calls (ns)."""
         import torch
         if on:
-            self._prof = torch.zeros(8, dtype=torch.float64, device="cuda")
+            self._prof = torch.zeros(16, dtype=torch.float64, device="cuda")
             ptr = _lib.ptr(self._prof)
         else:
             self._prof = None
