@@ -804,7 +804,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     {
       InVec in{wy, nullptr, 0.0};
       EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r};
+      if (a.prof && threadIdx.x == 0) cgb_tl_acc = a.prof + 16;
       apply_plan(Aj, in, e, s, gs);
+      if (a.prof && threadIdx.x == 0) cgb_tl_acc = nullptr;
       gs.reduce(s);
     }
     prof.mark(PROF_RHS);

@@ -147,6 +147,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// run_level timeline probe (profiling only): when cgb_tl_acc != null, warp 0
+// of block 0 adds its per-tile phase times (ns) to cgb_tl_acc[0..7]
+__shared__ double* cgb_tl_acc;
+
 // per-warp pair of mbarriers for the double-buffered conv windows, and the
 // parity each buffer's next completion will have (bit b for buffer b)
 __shared__ uint64_t cgb_mbar[CGB_WARPS][2];
@@ -161,6 +165,7 @@ __device__ __forceinline__ void tma_init() {
     cgb_mbar_phase[wib] = 0;
     fence_mbar_init();
   }
+  if (threadIdx.x == 0) cgb_tl_acc = nullptr;
   __syncthreads();
 }
 
@@ -444,9 +449,15 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
                                           double* xs, double* os) {
   switch (L.kind) {
     case CGB_LEAF_IDENTITY: {
+      double v[CGB_RC];
+#pragma unroll
+      for (int r = 0; r < CGB_RC; ++r) {  // clamped: every load in flight at once
+        const int rr = lane + 32 * r;
+        v[r] = in(lrow0 + (r < R && rr < nvalid ? rr : 0));
+      }
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r)
-        if (r < R && lane + 32 * r < nvalid) acc[r] += alpha * in(lrow0 + lane + 32 * r);
+        if (r < R && lane + 32 * r < nvalid) acc[r] += alpha * v[r];
     } break;
     case CGB_LEAF_DENSE: {
       double mine[CGB_RC];
@@ -656,6 +667,8 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
     win = conv_window(P, rb, row0, in, temp);
     if (win.ok) issue_window(win, xsb0, &bar[0], lane);
   }
+  double* tl = (blockIdx.x == 0 && wib == 0 && lane == 0) ? cgb_tl_acc : nullptr;
+  uint64_t tl0 = tl ? globaltimer() : 0, tl1 = tl0;
   for (; tile < T; tile += stride) {
     const DevRowBlock rb = P.rbs[rbi];
     const int R = rb.rfac;
@@ -684,10 +697,13 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       const double* cc = toff >= 0 ? P.taps + toff : nullptr;
       if (t == rb.conv_term && win.ok) {
         // the window was issued one tile ago; wait for its bytes
+        if (tl) { const uint64_t x = globaltimer(); tl[3] += (double)(x - tl1); tl1 = x; }
         mbar_wait(&bar[cur], (ph >> cur) & 1u);
         ph ^= 1u << cur;
         __syncwarp();
+        if (tl) { const uint64_t x = globaltimer(); tl[1] += (double)(x - tl1); tl1 = x; }
         conv_compute(L.k0, xcur + win.shift, cc, os, acc, tm.alpha, nvalid, lane);
+        if (tl) { const uint64_t x = globaltimer(); tl[2] += (double)(x - tl1); tl1 = x; }
         continue;
       }
       const InVec tin = tm.in_buf == 0
@@ -695,6 +711,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
                             : InVec{temp + P.temp_off[tm.in_buf - 1] + tm.in_off, nullptr, 0.0};
       leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os);
     }
+    if (tl) { const uint64_t x = globaltimer(); tl[3] += (double)(x - tl1); tl1 = x; }
     if (rb.out_buf == 0) {
       epi.tile(row0 + lane, row0, R, nvalid - lane, acc, part);
     } else {
@@ -703,11 +720,18 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       for (int r = 0; r < CGB_RC; ++r)
         if (r < R && lane + 32 * r < nvalid) dst[32 * r] = acc[r];
     }
+    if (tl) {
+      const uint64_t x = globaltimer();
+      tl[4] += (double)(x - tl1);
+      tl1 = x;
+      tl[0] += 1.0;
+    }
     cur ^= 1;
     rbi = nrbi;
     row0 = nrow0;
     win = nwin;
   }
+  if (tl) tl[5] += (double)(globaltimer() - tl0);
   __syncwarp();
   if (lane == 0) cgb_mbar_phase[wib] = ph;
   __syncwarp();

@@ -319,7 +319,7 @@ class SolverPlan:
         """Accumulate per-phase device time of later run() calls (ns)."""
         import torch
         if on:
-            self._prof = torch.zeros(16, dtype=torch.float64, device="cuda")
+            self._prof = torch.zeros(32, dtype=torch.float64, device="cuda")
             ptr = _lib.ptr(self._prof)
         else:
             self._prof = None
@@ -329,7 +329,12 @@ class SolverPlan:
     def profile(self) -> dict:
         """Seconds spent per phase since enable_profile()."""
         vals = self._prof.cpu().numpy() * 1e-9
-        return {nm: float(vals[i]) for i, nm in enumerate(self.PROFILE_PHASES)}
+        out = {nm: float(vals[i]) for i, nm in enumerate(self.PROFILE_PHASES)}
+        tl = vals[16:24]
+        out["rhs_warp0_timeline"] = {"tiles": float(tl[0] * 1e9), "tma_wait": float(tl[1]),
+                                     "conv": float(tl[2]), "other_terms": float(tl[3]),
+                                     "epilogue": float(tl[4]), "level_total": float(tl[5])}
+        return out
 
     def loop_vars(self) -> list:
         st = self.state()

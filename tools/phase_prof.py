@@ -32,7 +32,10 @@ done = int(st[_lib.ST_K]) - 20
 prof = plan.profile()
 out = {"n": n, "iters": done, "cg_iters": int(st[_lib.ST_CGT]), "ms": ms,
        "us_per_iter": 1e3 * ms / max(done, 1),
-       "phase_us_per_iter": {k: 1e6 * v / max(done, 1) for k, v in prof.items()}}
+       "phase_us_per_iter": {k: 1e6 * v / max(done, 1) for k, v in prof.items()
+                             if not isinstance(v, dict)},
+       "rhs_warp0_timeline_us_per_iter": {k: (v if k == "tiles" else 1e6 * v) / max(done, 1)
+                                          for k, v in prof["rhs_warp0_timeline"].items()}}
 print(json.dumps(out, indent=1))
 plan.enable_profile(False)
 plan.reset()
