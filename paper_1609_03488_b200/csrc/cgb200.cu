@@ -45,20 +45,29 @@ struct EpiStore {  // y -> out
 // Splitting-step / inner-solve start: with y = A^T d2 and g = A^T A x0,
 //   rhs = d1 - y ;  r = rhs - (x0 + g) ;  sums: rhs.rhs, r.r (+ c.x0)
 // (scs.py:349 rhs = wz1 - A^T wz2 ; cg.py:129 r0 = b - (1*x + A^T A x))
+//   dw != null: d1 is not in memory but d1 = x0 - tau_w dw (the splitting
+//   solver's w_x = u~_x = p1 - tau~ g_x of the previous cone step, computed
+//   with the same fused multiply-add as XStep, so bitwise identical)
 struct EpiRhs {
   const double* d1;
   const double* x0;
   const double* g;
   const double* c;  // optional: slot 2 gets c.x0
   double* r;
+  const double* dw;
+  double tau_w;
   __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double a[CGB_RC], x[CGB_RC], gg[CGB_RC], cc[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       const int64_t jq = CGB_EPI_IDX(j, q);
-      a[q] = d1[jq]; x[q] = x0[jq]; gg[q] = g[jq];
+      a[q] = dw ? dw[jq] : d1[jq]; x[q] = x0[jq]; gg[q] = g[jq];
       if (c) cc[q] = c[jq];
+    }
+    if (dw) {
+#pragma unroll
+      for (int q = 0; q < CGB_RC; ++q) a[q] = fma(-tau_w, a[q], x[q]);
     }
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
@@ -597,7 +606,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_cons
   double s[3] = {0.0, 0.0, 0.0};
   {
     InVec din{a.d2, nullptr, 0.0};
-    EpiRhs e{a.d1, z1, a.gx, nullptr, a.r};
+    EpiRhs e{a.d1, z1, a.gx, nullptr, a.r, nullptr, 0.0};
     apply_plan(Aj, din, e, s, gs);
     gs.reduce(s);
   }
@@ -703,7 +712,7 @@ struct ConeElem {
 struct XStep {
   double* u; double* w; double tau; int write_u;
   __device__ __forceinline__ void compute(int64_t i, const double (&v)[2], int64_t) {
-    const double ut = v[0] - tau * v[1];
+    const double ut = fma(-tau, v[1], v[0]);
     w[i] = ut;
     if (write_u) u[i] = ut;
   }
@@ -779,6 +788,8 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
   // running scalars: b.(A x) follows x through the CG updates; b.w_y is
   // summed by every cone step for the next subspace step.
   double bax = 0.0, bwy_part = 0.0;
+  bool wx_stale = false;  // w_x not stored since the last cone step
+  double tau_prev = 0.0;  // that cone step's tau~
   {
     double s[2] = {0.0, 0.0};
     s[0] = side_dot(m, a.b, W.tax);
@@ -803,7 +814,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double s[4] = {0.0, 0.0, 0.0, bwy_part};
     {
       InVec in{wy, nullptr, 0.0};
-      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r};
+      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev};
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = a.prof + 16;
       apply_plan(Aj, in, e, s, gs);
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = nullptr;
@@ -828,11 +839,15 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double red[2 * CGB_MAX_LARGE_SOC];
 #pragma unroll
     for (int i = 0; i < 2 * CGB_MAX_LARGE_SOC; ++i) red[i] = 0.0;
-    {
+    // w_x = u_x = p1 - tau~ g_x: stored only when u is (check / last
+    // iteration / trace); otherwise the next rhs epilogue recomputes it
+    if (write_u) {
       XStep fx{W.u, W.w, tau_t, write_u};
       const double* src[2] = {W.cgx, a.g};
       bulk_stream<2>(n, src, fx);
     }
+    wx_stale = !write_u;
+    tau_prev = tau_t;
     if (a.prof) {  // profiling only: separate the sub-phases
       gs.sync();
       prof.mark(PROF_CONE_X);
@@ -894,7 +909,14 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
         gs.sync();
         prof.mark(PROF_CONE_A);
       }
-      gs.reduce(red);
+      if (K.nlarge == 1) {  // the common case: reduce just (tail^2, head)
+        double r2[2] = {red[0], red[1]};
+        gs.reduce(r2);
+        red[0] = r2[0];
+        red[1] = r2[1];
+      } else {
+        gs.reduce(red);
+      }
       prof.mark(PROF_CONE_AR);
       if (a.prof) {  // profiling only: the same reduction again, warm
         double red2[2 * CGB_MAX_LARGE_SOC];

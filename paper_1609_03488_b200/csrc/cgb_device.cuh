@@ -17,7 +17,7 @@
 #endif
 #define CGB_MAXP 16          // reduction slots per grid reduction
 #ifndef CGB_BAR_FENCE
-#define CGB_BAR_FENCE 2      // grid-barrier fence flavour (see GridSync::sync)
+#define CGB_BAR_FENCE 1      // grid-barrier fence flavour (see GridSync::sync)
 #endif
 #define CGB_MAXG 160         // largest grid the reductions are unrolled for (148 SMs x 1)
 #define CGB_MAX_LARGE_SOC 4  // SOC blocks reduced across the whole grid
