@@ -9,7 +9,7 @@
 #include "../../include/cgb200.h"
 
 #ifndef CGB_BLOCK
-#define CGB_BLOCK 512
+#define CGB_BLOCK 256
 #endif
 #define CGB_WARPS (CGB_BLOCK / 32)
 #ifndef CGB_MINB
@@ -25,7 +25,7 @@
 #define CGB_RC 9             // rows per lane in convolution tiles (odd: no bank conflicts)
 #endif
 #define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
-#define CGB_U 4              // elements per thread per batch in streaming loops
+#define CGB_U 8              // elements per thread per batch in streaming loops
 
 namespace cgb {
 
