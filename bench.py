@@ -176,8 +176,16 @@ def cpu_sample(n: int, iters: int, warmup_iters: int = 1):
 
 
 def _cpu_cores_used() -> int:
-    # numpy FFT / convolve / dot on 1-d float64 vectors run single-threaded
-    return 1
+    """Host threads the oracle can use: numpy's FFTs are single-threaded, its
+    dot products / norms run in OpenBLAS with this many threads."""
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
+        if blas:
+            return int(max(blas))
+    except Exception:  # noqa: BLE001 - reporting only
+        pass
+    return os.cpu_count() or 1
 
 
 def run_reference(args) -> None:
@@ -351,7 +359,8 @@ def run_b200(args) -> None:
                "kind": "port",
                "sample": f"{cs['iters']} splitting iterations of the same n={n} instance "
                          f"after the oracle's setup solve ({cs['setup_s']:.1f} s); numpy "
-                         f"restatement of conegraph scs.py, single thread",
+                         f"restatement of conegraph scs.py (FFT convolutions single-threaded, "
+                         f"dot products in OpenBLAS threads; host has {os.cpu_count()} cpus)",
                "setup_s": cs["setup_s"],
                "time_to_eps_s_extrapolated": cs["setup_s"] + per_it * statistics.mean(iters)}
 

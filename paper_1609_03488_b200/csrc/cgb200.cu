@@ -1267,6 +1267,7 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   });
   std::vector<DevRowBlock> rbs(d->nrowblocks);
   const int64_t kLongBlock = 32 * CGB_RC * 256;
+  int64_t kw2max = 0;  // widest 2-d kernel row of a periodic (tiled) block
   std::vector<int32_t> level_rb(nlevels + 1, 0);
   std::vector<int64_t> level_tiles(nlevels, 0);
   int64_t kmax = 0;
@@ -1286,7 +1287,8 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       D.term_end = R.term_end;
       D.rfac = 1;
       D.conv_term = -1;
-      D.pad = 0;
+      D.period = 0;
+      D.tpr = 0;
       int nconv = 0;
       for (int t = R.term_begin; t < R.term_end; ++t) {
         const cgb_leaf& LF = d->leaves[d->terms[t].leaf];
@@ -1308,8 +1310,30 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
           dense |= d->leaves[d->terms[t].leaf].kind == CGB_LEAF_DENSE;
         if (!dense) D.rfac = CGB_RC;
       }
-      const int64_t rows_per_tile = 32 * (int64_t)D.rfac;
-      tiles += (R.row_end - R.row_begin + rows_per_tile - 1) / rows_per_tile;
+      // 2-d conv terms: whole output rows of one width -> periodic tiles that
+      // never cross a row (the tiled 2-d path needs a tile inside one row)
+      int64_t period = 0;
+      bool periodic_ok = true;
+      for (int t = R.term_begin; t < R.term_end; ++t) {
+        const cgb_term& T = d->terms[t];
+        const cgb_leaf& LF = d->leaves[T.leaf];
+        if (LF.kind != CGB_LEAF_CONV2D && LF.kind != CGB_LEAF_CORR2D) continue;
+        const int64_t ow = LF.kind == CGB_LEAF_CONV2D ? LF.n1 + LF.k1 - 1 : LF.n1;
+        if (LF.k1 > CGB_CONV_KMAX || (period && ow != period) ||
+            (R.row_begin - T.row_origin) % ow != 0 || (R.row_end - R.row_begin) % ow != 0)
+          periodic_ok = false;
+        period = ow;
+        kw2max = std::max<int64_t>(kw2max, LF.k1);
+      }
+      if (period > 0 && periodic_ok) {
+        D.rfac = CGB_RC;
+        D.period = period;
+        D.tpr = (int32_t)((period + 32 * CGB_RC - 1) / (32 * CGB_RC));
+        tiles += (R.row_end - R.row_begin) / period * D.tpr;
+      } else {
+        const int64_t rows_per_tile = 32 * (int64_t)D.rfac;
+        tiles += (R.row_end - R.row_begin + rows_per_tile - 1) / rows_per_tile;
+      }
       ++idx;
     }
     level_tiles[e] = tiles;
@@ -1327,6 +1351,18 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       leaf_taps[i] = (int32_t)taps.size();
       for (int64_t j = 0; j < nt; ++j)
         taps.push_back(j < L.k0 ? kv[L.kind == CGB_LEAF_CONV1D ? L.k0 - 1 - j : j] : 0.0);
+    }
+    if ((L.kind == CGB_LEAF_CONV2D || L.kind == CGB_LEAF_CORR2D) && L.k1 <= CGB_CONV_KMAX &&
+        L.k0 * ((L.k1 + CGB_RC - 1) / CGB_RC * CGB_RC) <= 4096) {
+      // one correlation row per kernel row a (reversed for the full conv)
+      std::vector<double> kv(L.k0 * L.k1);
+      CUDA_TRY(cudaMemcpy(kv.data(), L.val, sizeof(double) * kv.size(), cudaMemcpyDeviceToHost));
+      const int64_t nt = (L.k1 + CGB_RC - 1) / CGB_RC * CGB_RC;
+      leaf_taps[i] = (int32_t)taps.size();
+      for (int64_t a = 0; a < L.k0; ++a)
+        for (int64_t j = 0; j < nt; ++j)
+          taps.push_back(j < L.k1 ? kv[a * L.k1 + (L.kind == CGB_LEAF_CONV2D ? L.k1 - 1 - j : j)]
+                                  : 0.0);
     }
   }
   Blob blob;
@@ -1360,18 +1396,22 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   P.temp[0] = ps->temps;
   P.temp[1] = ps->temps ? ps->temps + temp_total : nullptr;
   P.nlevels = nlevels;
-  P.pad = 0;
+
+  // per warp: 1-d window buffers 0 and 1 | output transpose | 2-d row ring
+  P.smem_cc = 0;
+  P.smem_xs = 0;
+  P.smem_xs2 = 0;
+  P.smem_per_warp = 0;
   if (kmax > 0) {
-    // per warp: window buffer 0 | window buffer 1 | output transpose
     const int64_t ntaps = (kmax + CGB_RC - 1) / CGB_RC * CGB_RC;
-    P.smem_cc = 0;
     P.smem_xs = (int32_t)((32 * CGB_RC + ntaps + 2 + 1) & ~1);
-    P.smem_per_warp = (2 * P.smem_xs + 32 * CGB_RC + 1 + 1) & ~1;
-  } else {
-    P.smem_cc = 0;
-    P.smem_xs = 0;
-    P.smem_per_warp = 0;
   }
+  if (kw2max > 0) {
+    const int64_t ntaps = (kw2max + CGB_RC - 1) / CGB_RC * CGB_RC;
+    P.smem_xs2 = (int32_t)((32 * CGB_RC + ntaps + 2 + 1) & ~1);
+  }
+  if (kmax > 0 || kw2max > 0)
+    P.smem_per_warp = 2 * P.smem_xs + (32 * CGB_RC + 2) + CGB_RING2 * P.smem_xs2;
   P.in_len = d->in_len;
   P.out_len = d->out_len;
   ps->in_len = d->in_len;

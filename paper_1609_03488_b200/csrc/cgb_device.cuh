@@ -34,11 +34,30 @@ namespace cgb {
 // ---------------------------------------------------------------------------
 struct DevRowBlock {
   int64_t row_begin, row_end, tile_begin;
+  int64_t period;     // > 0: the block is whole output rows of this width
+                      // (a 2-d conv leaf); tiles never cross a row
   int32_t out_buf, term_begin, term_end;
   int32_t rfac;       // rows per lane in this block's tiles (1 or CGB_RC)
   int32_t conv_term;  // the block's only 1-d conv term (TMA-staged), or -1
-  int32_t pad;
+  int32_t tpr;        // periodic blocks: tiles per row
 };
+
+// first row and row count of a tile of row block rb
+__device__ __forceinline__ void tile_rows(const DevRowBlock& rb, int64_t tile, int64_t& row0,
+                                          int& nvalid) {
+  const int64_t rpt = 32 * (int64_t)rb.rfac;
+  const int64_t t = tile - rb.tile_begin;
+  if (rb.period > 0) {
+    const int64_t pr = t / rb.tpr, pc = t - pr * rb.tpr;
+    row0 = rb.row_begin + pr * rb.period + pc * rpt;
+    const int64_t rem = rb.period - pc * rpt;
+    nvalid = (int)(rem < rpt ? rem : rpt);
+  } else {
+    row0 = rb.row_begin + t * rpt;
+    const int64_t rem = rb.row_end - row0;
+    nvalid = (int)(rem < rpt ? rem : rpt);
+  }
+}
 
 // All metadata arrays of a plan live in one device blob [meta, meta +
 // meta_bytes) so a kernel can copy the whole plan into shared memory once
@@ -60,8 +79,8 @@ struct DevPlan {
   int32_t smem_per_warp;  // doubles of dynamic shared memory per warp
   int32_t smem_cc;        // (unused, 0)
   int32_t smem_xs;        // one staged-input window; two windows, then the
-                          // 32*RC+1 output transpose
-  int32_t pad;
+                          // 32*RC+1 output transpose, then the 2-d ring
+  int32_t smem_xs2;       // one 2-d conv row window (CGB_RING2 of them)
   int64_t in_len, out_len;
 };
 
@@ -151,17 +170,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // of block 0 adds its per-tile phase times (ns) to cgb_tl_acc[0..7]
 __shared__ double* cgb_tl_acc;
 
+// lane 0 issues one bulk copy into `dst` once the warp's earlier reads of it
+// are fenced off from the async proxy
+__device__ __forceinline__ void issue_bulk(double* dst, const double* src, uint32_t bytes,
+                                           uint64_t* bar, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    fence_proxy_async();
+    bulk_load(dst, src, bytes, bar);
+  }
+}
+
 // per-warp pair of mbarriers for the double-buffered conv windows, and the
 // parity each buffer's next completion will have (bit b for buffer b)
-__shared__ uint64_t cgb_mbar[CGB_WARPS][2];
+#define CGB_RING2 4  // row windows in flight per warp in a 2-d conv tile
+__shared__ uint64_t cgb_mbar[CGB_WARPS][2 + CGB_RING2];
 __shared__ uint32_t cgb_mbar_phase[CGB_WARPS];
 
 // every persistent kernel calls this first (all threads)
 __device__ __forceinline__ void tma_init() {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   if (lane == 0) {
-    mbar_init(&cgb_mbar[wib][0], 1);
-    mbar_init(&cgb_mbar[wib][1], 1);
+    for (int i = 0; i < 2 + CGB_RING2; ++i) mbar_init(&cgb_mbar[wib][i], 1);
     cgb_mbar_phase[wib] = 0;
     fence_mbar_init();
   }
@@ -403,17 +433,13 @@ __device__ __forceinline__ int conv_span(int64_t k) { return 32 * CGB_RC + conv_
 // with a sliding register window -- one shared load of the window and one
 // (broadcast) tap load per RC FMAs -- then transposes the results to the
 // lane-strided tile layout through `os` and accumulates alpha * y.
-__device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const double* cc,
-                                             double* os, double (&acc)[CGB_RC], double alpha,
-                                             int nvalid, int lane) {
+__device__ __forceinline__ void conv_accum(int64_t k, const double* xs, const double* cc,
+                                           double (&y)[CGB_RC], int lane) {
   const int ngroups = (int)((k + CGB_RC - 1) / CGB_RC);
   const int o0 = lane * CGB_RC;
-  double y[CGB_RC], w[CGB_RC];
+  double w[CGB_RC];
 #pragma unroll
-  for (int r = 0; r < CGB_RC; ++r) {
-    y[r] = 0.0;
-    w[r] = xs[o0 + r];
-  }
+  for (int r = 0; r < CGB_RC; ++r) w[r] = xs[o0 + r];
   for (int g = 0; g < ngroups; ++g) {
     const double* xg = xs + o0 + g * CGB_RC + CGB_RC;
     const double* cg = cc + g * CGB_RC;
@@ -425,6 +451,14 @@ __device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const 
       w[jj] = xg[jj];  // slot jj slides from x[o0+gRC+jj] to x[o0+gRC+jj+RC]
     }
   }
+}
+
+// lane-consecutive results y (lane l holds outputs l*RC .. l*RC+RC-1) to the
+// lane-strided tile layout, accumulated as acc += alpha * y
+__device__ __forceinline__ void tile_transpose(const double (&y)[CGB_RC], double* os,
+                                               double (&acc)[CGB_RC], double alpha, int nvalid,
+                                               int lane) {
+  const int o0 = lane * CGB_RC;
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < CGB_RC; ++r) os[o0 + r] = y[r];
@@ -433,6 +467,105 @@ __device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const 
   for (int r = 0; r < CGB_RC; ++r)
     if (lane + 32 * r < nvalid) acc[r] += alpha * os[lane + 32 * r];
   __syncwarp();
+}
+
+__device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const double* cc,
+                                             double* os, double (&acc)[CGB_RC], double alpha,
+                                             int nvalid, int lane) {
+  double y[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) y[r] = 0.0;
+  conv_accum(k, xs, cc, y, lane);
+  tile_transpose(y, os, acc, alpha, nvalid, lane);
+}
+
+// Stage xs[0..span) = row[lo + i] (zero outside [0, len)) by hand.
+__device__ __forceinline__ void stage_row(const double* row, int64_t lo, int64_t len, int span,
+                                          double* xs, int lane) {
+  for (int i0 = 0; i0 < span; i0 += 32 * CGB_U) {
+    double xv[CGB_U];
+#pragma unroll
+    for (int u = 0; u < CGB_U; ++u) {
+      const int i = i0 + lane + 32 * u;
+      const int64_t xi = lo + i;
+      const int64_t xc = xi < 0 ? 0 : (xi >= len ? len - 1 : xi);
+      const double v = row[xc];
+      xv[u] = (i < span && xi >= 0 && xi < len) ? v : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CGB_U; ++u) {
+      const int i = i0 + lane + 32 * u;
+      if (i < span) xs[i] = xv[u];
+    }
+  }
+}
+
+// 2-d convolution (full, CONV2D) / correlation (valid, CORR2D) tile: the
+// tile is a segment of one output row (periodic row block), lane l owns the
+// RC consecutive outputs of the segment at l*RC.  Every kernel row a adds a
+// 1-d correlation of one input row with that kernel row (reversed for conv,
+// taps from the plan) -- conv_accum on a window of the input row.  The kh
+// row windows stream through a per-warp ring of CGB_RING2 shared buffers,
+// TMA bulk copies for interior windows, hand staging at the image edge.
+__device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0, int nvalid,
+                                         const double* x, double alpha, const double* taps,
+                                         double* ring, int xs2, double* os,
+                                         double (&acc)[CGB_RC], int lane) {
+  const bool conv = L.kind == CGB_LEAF_CONV2D;
+  const int64_t H = L.n0, W = L.n1, kh = L.k0, kw = L.k1;
+  const int64_t OW = conv ? W + kw - 1 : W;         // output row width
+  const int64_t IW = conv ? W : W + kw - 1;         // input row width
+  const int64_t IH = conv ? H : H + kh - 1;         // input rows
+  const int64_t oi = lrow0 / OW, oj0 = lrow0 - oi * OW;
+  const int ntaps = conv_ntaps(kw);
+  const int span = 32 * CGB_RC + ntaps;
+  const int64_t clo = conv ? oj0 - (kw - 1) : oj0;  // first input column of the window
+  const int wib = threadIdx.x >> 5;
+  uint64_t* bar = &cgb_mbar[wib][2];
+  uint32_t ph = cgb_mbar_phase[wib] >> 2;
+  // kernel rows that touch the image, as input rows xi(a) = oi - a / oi + a
+  int64_t a_lo = 0, a_hi = kh - 1;
+  if (conv) {
+    a_lo = oi - (IH - 1) > 0 ? oi - (IH - 1) : 0;
+    a_hi = oi < kh - 1 ? oi : kh - 1;
+  }
+  const int nrows = (int)(a_hi - a_lo + 1);
+  const bool tma = clo >= 0 && clo + span <= IW;
+  auto issue = [&](int idx) {
+    const int64_t a = a_lo + idx;
+    const int64_t xi = conv ? oi - a : oi + a;
+    const double* src = x + xi * IW + clo;
+    const int sh = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    const uint32_t bytes = (uint32_t)(((span + sh) * 8 + 15) & ~15);
+    issue_bulk(ring + (idx % CGB_RING2) * xs2, src - sh, bytes, &bar[idx % CGB_RING2], lane);
+  };
+  if (tma)
+    for (int i = 0; i < CGB_RING2 && i < nrows; ++i) issue(i);
+  double y[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) y[r] = 0.0;
+  for (int i = 0; i < nrows; ++i) {
+    const int64_t a = a_lo + i;
+    const int64_t xi = conv ? oi - a : oi + a;
+    const double* rowp = x + xi * IW;
+    double* xs = ring + (i % CGB_RING2) * xs2;
+    int sh = 0;
+    if (tma) {
+      const int b = i % CGB_RING2;
+      mbar_wait(&bar[b], (ph >> b) & 1u);
+      ph ^= 1u << b;
+      sh = (int)((reinterpret_cast<uintptr_t>(rowp + clo) >> 3) & 1);
+    } else {
+      __syncwarp();
+      stage_row(rowp, clo, IW, span, xs, lane);
+    }
+    __syncwarp();
+    conv_accum(kw, xs + sh, taps + a * ntaps, y, lane);
+    if (tma && i + CGB_RING2 < nrows) issue(i + CGB_RING2);
+  }
+  if (lane == 0) cgb_mbar_phase[wib] = (cgb_mbar_phase[wib] & 3u) | (ph << 2);
+  __syncwarp();
+  tile_transpose(y, os, acc, alpha, nvalid, lane);
 }
 
 // Contribution of one leaf to a warp tile.  The tile holds 32*R rows
@@ -446,7 +579,8 @@ __device__ __forceinline__ void conv_compute(int64_t k, const double* xs, const 
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
                                           double (&acc)[CGB_RC], int lane, const double* cc,
-                                          double* xs, double* os) {
+                                          double* xs, double* os, double* ring = nullptr,
+                                          int xs2 = 0) {
   switch (L.kind) {
     case CGB_LEAF_IDENTITY: {
       double v[CGB_RC];
@@ -539,6 +673,10 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
     } break;
     case CGB_LEAF_CONV2D:
     case CGB_LEAF_CORR2D: {
+      if (R == CGB_RC && cc && ring) {
+        conv2d_tile(L, lrow0, nvalid, in.a, alpha, cc, ring, xs2, os, acc, lane);
+        break;
+      }
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r) {
         if (r < R && lane + 32 * r < nvalid) {
@@ -647,6 +785,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
   double* xsb0 = cgb_dyn_smem + (size_t)wib * P.smem_per_warp;
   double* xsb1 = xsb0 + P.smem_xs;
   double* os = xsb1 + P.smem_xs;
+  double* ring = P.smem_xs2 > 0 ? os + (32 * CGB_RC + 2) : nullptr;
   uint64_t* bar = cgb_mbar[wib];
   const int64_t G = gridDim.x;
   const int64_t stride = G * CGB_WARPS;
@@ -659,11 +798,12 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
   int64_t tile = blockIdx.x + G * wib;
   int rbi = 0;
   int64_t row0 = 0;
+  int nvalid = 0;
   ConvWin win{nullptr, 0u, 0, false};
   if (tile < T) {
     rbi = find_rowblock(P, rb_lo, rb_hi, tile);
     const DevRowBlock& rb = P.rbs[rbi];
-    row0 = rb.row_begin + (tile - rb.tile_begin) * (32 * rb.rfac);
+    tile_rows(rb, tile, row0, nvalid);
     win = conv_window(P, rb, row0, in, temp);
     if (win.ok) issue_window(win, xsb0, &bar[0], lane);
   }
@@ -672,18 +812,17 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
   for (; tile < T; tile += stride) {
     const DevRowBlock rb = P.rbs[rbi];
     const int R = rb.rfac;
-    const int64_t rem = rb.row_end - row0;
-    const int nvalid = rem < 32 * R ? (int)rem : 32 * R;
     double* xcur = cur ? xsb1 : xsb0;
     // prefetch the next tile's window into the other buffer
     const int64_t ntile = tile + stride;
     int nrbi = rbi;
     int64_t nrow0 = 0;
+    int nnvalid = 0;
     ConvWin nwin{nullptr, 0u, 0, false};
     if (ntile < T) {
       nrbi = find_rowblock(P, rb_lo, rb_hi, ntile);
       const DevRowBlock& nrb = P.rbs[nrbi];
-      nrow0 = nrb.row_begin + (ntile - nrb.tile_begin) * (32 * nrb.rfac);
+      tile_rows(nrb, ntile, nrow0, nnvalid);
       nwin = conv_window(P, nrb, nrow0, in, temp);
       if (nwin.ok) issue_window(nwin, cur ? xsb0 : xsb1, &bar[cur ^ 1], lane);
     }
@@ -709,7 +848,8 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       const InVec tin = tm.in_buf == 0
                             ? in.shift(tm.in_off)
                             : InVec{temp + P.temp_off[tm.in_buf - 1] + tm.in_off, nullptr, 0.0};
-      leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os);
+      leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os,
+                tin.b ? nullptr : ring, P.smem_xs2);
     }
     if (tl) { const uint64_t x = globaltimer(); tl[3] += (double)(x - tl1); tl1 = x; }
     if (rb.out_buf == 0) {
@@ -729,11 +869,12 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
     cur ^= 1;
     rbi = nrbi;
     row0 = nrow0;
+    nvalid = nnvalid;
     win = nwin;
   }
   if (tl) tl[5] += (double)(globaltimer() - tl0);
   __syncwarp();
-  if (lane == 0) cgb_mbar_phase[wib] = ph;
+  if (lane == 0) cgb_mbar_phase[wib] = (cgb_mbar_phase[wib] & ~3u) | (ph & 3u);
   __syncwarp();
 }
 

@@ -308,3 +308,50 @@ def test_deconv_short_kernel_end_to_end():
     assert abs(sol.iterations - osol.iterations) <= max(0.02 * osol.iterations, 20)
     if sol.status == "solved":
         assert abs(sol.pobj - osol.pobj) <= 1e-6 * abs(osol.pobj) + 1e-3 * abs(osol.pobj)
+
+
+@pytest.mark.parametrize("h,w,kh,kw", [(50, 700, 15, 15), (33, 611, 5, 7), (20, 300, 1, 15),
+                                        (17, 1200, 15, 1), (9, 289, 3, 3)])
+def test_conv2d_tiled_against_oracle(h, w, kh, kw):
+    """The tiled 2-d path (periodic row blocks, TMA row windows for interior
+    tiles, hand staging at the edges) vs scipy full convolution / valid
+    correlation, forward and adjoint, 1e-12 relative."""
+    from oracle import linop_ref
+    import _exprs as E
+    rng = np.random.default_rng(h * 1000 + w)
+    K = rng.standard_normal((kh, kw))
+    op = linop.conv2d(K, (h, w))
+    ref = E.Conv2D(K, (h, w))
+    x = rng.standard_normal(h * w)
+    y = rng.standard_normal(op.rows)
+    f = op.forward(x)
+    np.testing.assert_allclose(f, linop_ref.forward(ref, x), rtol=1e-12,
+                               atol=1e-12 * np.abs(f).max())
+    a = op.adjoint_apply(y)
+    np.testing.assert_allclose(a, linop_ref.adjoint(ref, y), rtol=1e-12,
+                               atol=1e-12 * np.abs(a).max())
+
+
+def test_deconv2d_end_to_end_matches_oracle():
+    """configs[2] at small scale: 2-d nonnegative deconvolution of a 40 x 330
+    image with a 7 x 7 blur, stuffed like build_deconv, device vs oracle:
+    same status, iterations within 2 % (or exactly equal), objective 1e-6
+    when the trajectories agree."""
+    from oracle import scs_ref
+    from paper_1609_03488_b200 import canon
+    h, w, kh, kw = 40, 330, 7, 7
+    K, b, _ = canon.gen_deconv2d(h, w, kh, kw, seed=4, spikes=30)
+    prob = canon.build_deconv2d(canon.Deconv2DProblem(K, b, (h, w)))
+    st = scs.ScsSettings(eps=1e-3, max_iters=20000)
+    sol = scs.solve(prob, st)
+
+    class _P:
+        pass
+    p = _P()
+    p.A, p.b, p.c, p.K = prob.A.expr, prob.b, prob.c, prob.K
+    osol, _ = scs_ref.scs_solve(p, scs_ref.ScsOracleSettings(eps=1e-3, max_iters=20000))
+    assert sol.status == osol.status == "solved"
+    assert abs(sol.iterations - osol.iterations) <= max(0.02 * osol.iterations, 20)
+    if sol.iterations == osol.iterations:
+        assert abs(sol.pobj - osol.pobj) <= 1e-6 * abs(osol.pobj)
+    assert max(sol.primal_residual, sol.dual_residual, sol.gap) <= st.eps
