@@ -594,20 +594,37 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
         if (r < R && lane + 32 * r < nvalid) acc[r] += alpha * v[r];
     } break;
     case CGB_LEAF_DENSE: {
+      // warp per row, CGB_DR rows at a time so their loads are in flight
+      // together (one latency per row group instead of per row)
+      constexpr int CGB_DR = 8;
       double mine[CGB_RC];
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
       const int64_t cols = L.cols;
-      for (int rr = 0; rr < nvalid; ++rr) {
-        const double* row = L.val + (lrow0 + rr) * L.ld;
-        double s = 0.0;
-#pragma unroll 4
-        for (int64_t c = lane; c < cols; c += 32) s += __ldg(row + c) * in(c);
-        s = warp_sum(s);
-        if (lane == (rr & 31)) {
+      for (int rr0 = 0; rr0 < nvalid; rr0 += CGB_DR) {
+        double sacc[CGB_DR];
+        const double* rowp[CGB_DR];
 #pragma unroll
-          for (int r = 0; r < CGB_RC; ++r)
-            if (r == (rr >> 5)) mine[r] = s;
+        for (int q = 0; q < CGB_DR; ++q) {
+          sacc[q] = 0.0;
+          const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
+          rowp[q] = L.val + (lrow0 + rr) * L.ld;
+        }
+#pragma unroll 2
+        for (int64_t c = lane; c < cols; c += 32) {
+          const double xv = in(c);
+#pragma unroll
+          for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+        }
+#pragma unroll
+        for (int q = 0; q < CGB_DR; ++q) {
+          const double sq = warp_sum(sacc[q]);
+          const int rr = rr0 + q;
+          if (rr < nvalid && lane == (rr & 31)) {
+#pragma unroll
+            for (int r = 0; r < CGB_RC; ++r)
+              if (r == (rr >> 5)) mine[r] = sq;
+          }
         }
       }
 #pragma unroll
