@@ -10,6 +10,8 @@ are evidence for DESIGN.md; the driver runs the default):
   deconv1d      configs[1]  (default)
   deconv2d      configs[2]  2-d nonneg deconvolution 4096 x 4096, 15 x 15 blur
   lasso_sparse  configs[3]  sparse lasso A 8e6 x 1e6 CSR, density 1e-5 (1 GPU)
+  logreg        configs[4]  l1 logistic regression, 2 exp cones per sample, A 2e5 x 2e3
+  soc_ls        configs[4]  SOC-constrained least squares, dense A 2e5 x 2e3
 
 A *step* is one complete solve to eps from a cold start: the one-time
 setup solve g = (I+Q_z)^{-1} h followed by the splitting iterations until
@@ -233,6 +235,68 @@ class LassoSparse(Workload):
         return 12 * A.nnz + 8 * (self.n + 1) + 8 * (2 * self.m + 4 * self.n)
 
 
+class LogReg(Workload):
+    name = "logreg_exp"
+
+    def __init__(self, m: int = 200_000, n: int = 2_000, lam: float = 0.01):
+        self.m, self.n, self.lam = m, n, lam
+        self._d = None
+
+    def data(self):
+        if self._d is None:
+            from paper_1609_03488_b200 import canon
+            A, y, _ = canon.gen_logreg(self.m, self.n, seed=SEED)
+            self._d = (A, y)
+        return self._d
+
+    def config(self):
+        from paper_1609_03488_b200 import canon
+        ns, ms = canon.logreg_dims(self.m, self.n)
+        return {"workload": self.name, "baseline_config": 4, "A": [self.m, self.n],
+                "lam": self.lam, "exp_cones": 2 * self.m, "eps": self.eps, "stuffed_n": ns,
+                "stuffed_m": ms, "seed": SEED}
+
+    def problem(self):
+        from paper_1609_03488_b200 import canon
+        A, y = self.data()
+        return canon.build_logreg(canon.LogRegProblem(A, y, self.lam))
+
+    def h2d_bytes(self):
+        from paper_1609_03488_b200 import canon
+        ns, ms = canon.logreg_dims(self.m, self.n)
+        return 8 * (2 * self.m * self.n) + 12 * 6 * self.m + 8 * (ns + ms)
+
+
+class SocLs(Workload):
+    name = "soc_ls"
+
+    def __init__(self, m: int = 200_000, n: int = 2_000, radius: float = 1.0):
+        self.m, self.n, self.radius = m, n, radius
+        self._d = None
+
+    def data(self):
+        if self._d is None:
+            import numpy as np
+            rng = np.random.default_rng(SEED)
+            A = rng.standard_normal((self.m, self.n)) / np.sqrt(self.m)
+            b = A @ rng.standard_normal(self.n) + 0.1 * rng.standard_normal(self.m) / np.sqrt(self.m)
+            self._d = (A, b)
+        return self._d
+
+    def config(self):
+        return {"workload": self.name, "baseline_config": 4, "A": [self.m, self.n],
+                "radius": self.radius, "eps": self.eps, "stuffed_n": self.n + 1,
+                "stuffed_m": self.m + self.n + 2, "seed": SEED}
+
+    def problem(self):
+        from paper_1609_03488_b200 import canon, linop
+        A, b = self.data()
+        return canon.build_soc_ls(canon.SocLsProblem(linop.dense(A), b, self.radius))
+
+    def h2d_bytes(self):
+        return 8 * (2 * self.m * self.n + 2 * (self.m + self.n + 2) + self.n + 1)
+
+
 def make_workload(args) -> Workload:
     if args.workload == "deconv1d":
         return Deconv1D(args.n)
@@ -242,6 +306,10 @@ def make_workload(args) -> Workload:
         return LassoDense()
     if args.workload == "lasso_sparse":
         return LassoSparse()
+    if args.workload == "logreg":
+        return LogReg()
+    if args.workload == "soc_ls":
+        return SocLs()
     raise SystemExit(f"unknown workload {args.workload}")
 
 
@@ -252,7 +320,8 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="deconv1d",
-                    choices=["deconv1d", "deconv2d", "lasso_dense", "lasso_sparse"])
+                    choices=["deconv1d", "deconv2d", "lasso_dense", "lasso_sparse", "logreg",
+                             "soc_ls"])
     ap.add_argument("--n", type=int, default=N_SIGNAL, help="deconv1d signal length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -349,7 +418,7 @@ def _cpu_cores_used() -> int:
 
 def _default_cpu_iters(wl: Workload) -> int:
     return {"deconv1d_nonneg": 20, "deconv2d_nonneg": 2, "lasso_dense": 200,
-            "lasso_sparse": 3}.get(wl.name, 10)
+            "lasso_sparse": 3, "logreg_exp": 2, "soc_ls": 3}.get(wl.name, 10)
 
 
 def _oracle_cached(wl: Workload, own_setup: bool):
@@ -365,10 +434,8 @@ def _oracle_cached(wl: Workload, own_setup: bool):
         return p, s, cached, time.perf_counter() - t0
     from paper_1609_03488_b200 import scs
     pc = scs.prepare_subspace(wl.problem(), s.setup_cg_tol, s.cg_max_iter)
-    cached = scs_ref.Cached()
-    cached.h, cached.g = np.asarray(pc.h), np.asarray(pc.g)
-    cached.denom, cached.cg_tol, cached.cg_max_iter = pc.denom, s.setup_cg_tol, s.cg_max_iter
-    cached.setup_cg_iters = pc.setup_cg_iters
+    cached = scs_ref.Cached(np.asarray(pc.h), np.asarray(pc.g), float(pc.denom),
+                            s.setup_cg_tol, s.cg_max_iter, int(pc.setup_cg_iters))
     return p, s, cached, None
 
 

@@ -885,6 +885,16 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
         }
       }
     }
+    // exponential cones: a thread per cone, dual projection
+    for (int64_t cc = gtid(); cc < K.nexp; cc += gsize()) {
+      const int64_t off = K.exp_off[cc];
+      const double z0 = cs.src(off), z1 = cs.src(off + 1), z2 = cs.src(off + 2);
+      double p0 = z0, p1 = z1, p2 = z2;
+      exp_project_dual(p0, p1, p2);
+      bw += a.b[off] * cs.store(off, z0, p0);
+      bw += a.b[off + 1] * cs.store(off + 1, z1, p1);
+      bw += a.b[off + 2] * cs.store(off + 2, z2, p2);
+    }
     if (a.prof) {
       gs.sync();
       prof.mark(PROF_CONE_E);
@@ -1558,7 +1568,9 @@ int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, in
         }
         break;
       case CGB_CONE_EXP:
-        return fail(CGB_EINVAL, "exponential cone not supported by this build");
+        if (d != 3) return fail(CGB_EINVAL, "exponential cone has dimension 3");
+        exp_off.push_back(off);
+        break;
       default:
         return fail(CGB_EINVAL, "unknown cone kind");
     }

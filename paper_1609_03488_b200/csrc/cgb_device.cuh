@@ -949,6 +949,90 @@ struct SocCoef {
   }
 };
 
+// Exponential cone K_exp = cl{(x,y,z): y > 0, y e^{x/y} <= z}: projection of
+// one 3-vector, the same algorithm as oracle/expcone_ref.py (stationarity in
+// rho = x/y, roots of the e^{-2rho}-scaled equation G bracketed on a unit
+// grid over [-60, 40] and bisected; the root with s_p > 0, mu >= 0 or the
+// face point y = 0, whichever is closer).  A thread per cone.
+__device__ __forceinline__ double exp_g(double rho, double r, double s, double t) {
+  const double e1 = exp(-rho);
+  return (r - s * rho) * e1 * e1 + (r - r * rho - s) + t * e1 * (rho * rho - rho + 1.0);
+}
+
+__device__ void exp_project(double& r, double& s, double& t) {
+  // 1. inside K_exp
+  if (s > 0.0) {
+    if (r / s < 700.0 && s * exp(r / s) <= t) return;
+  } else if (r <= 0.0 && s == 0.0 && t >= 0.0) {
+    return;
+  }
+  // 2. inside the polar cone -> 0
+  if (r > 0.0) {
+    if (s / r < 700.0 && r * exp(s / r) + 2.718281828459045 * t <= 0.0) {
+      r = s = t = 0.0;
+      return;
+    }
+  } else if (r == 0.0 && s <= 0.0 && t <= 0.0) {
+    r = s = t = 0.0;
+    return;
+  }
+  // 3. the face y = 0
+  if (r < 0.0 && s < 0.0) {
+    s = 0.0;
+    t = fmax(t, 0.0);
+    return;
+  }
+  // 4. curved boundary (or the face)
+  double br = fmin(r, 0.0), bs = 0.0, bt = fmax(t, 0.0);
+  double bd = (r - br) * (r - br) + s * s + (t - bt) * (t - bt);
+  double lo = -60.0, glo = exp_g(lo, r, s, t);
+  while (lo < 40.0) {
+    const double hi = lo + 1.0;
+    const double ghi = exp_g(hi, r, s, t);
+    if ((glo < 0.0) != (ghi < 0.0) || ghi == 0.0) {
+      double a = lo, b = hi, ga = glo;
+      for (int it = 0; it < 64; ++it) {
+        const double mid = 0.5 * (a + b);
+        const double gm = exp_g(mid, r, s, t);
+        if ((gm < 0.0) == (ga < 0.0)) {
+          a = mid;
+          ga = gm;
+        } else {
+          b = mid;
+        }
+      }
+      const double rho = 0.5 * (a + b);
+      const double e = exp(rho);
+      const double sp = (r * rho + s + t * e) / (rho * rho + 1.0 + e * e);
+      const double mu = sp * e - t;
+      if (sp > 0.0 && mu >= -1e-12 * (1.0 + fabs(t))) {
+        const double px = sp * rho, py = sp, pz = sp * e;
+        const double d = (r - px) * (r - px) + (s - py) * (s - py) + (t - pz) * (t - pz);
+        if (d < bd) {
+          br = px;
+          bs = py;
+          bt = pz;
+          bd = d;
+        }
+      }
+    }
+    lo = hi;
+    glo = ghi;
+  }
+  r = br;
+  s = bs;
+  t = bt;
+}
+
+// Pi_{K_exp*}(v) = v + Pi_{K_exp}(-v)   (Moreau)
+__device__ __forceinline__ void exp_project_dual(double& r, double& s, double& t) {
+  double a = -r, b = -s, c = -t;
+  exp_project(a, b, c);
+  r += a;
+  s += b;
+  t += c;
+}
+
 template <class Src>
 struct SqSum {
   const Src* src;
@@ -1004,6 +1088,16 @@ __device__ void cone_project(const DevCones& K, int dual, const Src& src, const 
     SegProj<Src, Dst> f{&src, &dst, sg.begin, sg.kind, dual,
                         large ? SocCoef(t, sqrt(red[sg.slot])) : SocCoef(), t, {}};
     stream_loop(sg.end - sg.begin, f);
+  }
+  // exponential cones: a thread per cone
+  for (int64_t c = gtid(); c < K.nexp; c += gsize()) {
+    const int64_t off = K.exp_off[c];
+    double r = src(off), s = src(off + 1), t = src(off + 2);
+    if (dual) exp_project_dual(r, s, t);
+    else exp_project(r, s, t);
+    dst(off, r);
+    dst(off + 1, s);
+    dst(off + 2, t);
   }
   // small SOC blocks: one warp per cone
   const int lane = threadIdx.x & 31;

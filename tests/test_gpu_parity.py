@@ -355,3 +355,68 @@ def test_deconv2d_end_to_end_matches_oracle():
     if sol.iterations == osol.iterations:
         assert abs(sol.pobj - osol.pobj) <= 1e-6 * abs(osol.pobj)
     assert max(sol.primal_residual, sol.dual_residual, sol.gap) <= st.eps
+
+
+def test_exp_cone_projection_matches_oracle():
+    """Device exp-cone projection (k_cones) vs the oracle restatement, primal
+    and dual, on a product of many exp cones mixed with other factors."""
+    from oracle import expcone_ref as X
+    rng = np.random.default_rng(21)
+    ncone = 3000
+    K = cones.ConeProduct([cones.NonNegCone(5)] + [cones.ExpCone() for _ in range(ncone)] +
+                          [cones.SecondOrderCone(4)])
+    v = rng.standard_normal(K.total_dim) * np.exp(rng.uniform(-2, 2, K.total_dim))
+    p = cones.project_product(K, v)
+    pd = cones.project_product_dual(K, v)
+    for c in range(ncone):
+        blk = v[5 + 3 * c:8 + 3 * c]
+        sc = 1e-10 * (1.0 + np.linalg.norm(blk))
+        np.testing.assert_allclose(p[5 + 3 * c:8 + 3 * c], X.project_exp(blk), atol=sc)
+        np.testing.assert_allclose(pd[5 + 3 * c:8 + 3 * c], X.project_exp_dual(blk), atol=sc)
+    np.testing.assert_allclose(p[:5], np.maximum(v[:5], 0.0))
+
+
+def _oracle_problem(prob):
+    class _P:
+        pass
+    p = _P()
+    p.A, p.b, p.c, p.K = prob.A.expr, prob.b, prob.c, prob.K
+    return p
+
+
+def test_logreg_exp_cones_end_to_end():
+    """configs[4] (exp-cone logistic regression) at small scale: device vs
+    oracle, same status, objective within eps-level tolerance, and the
+    recovered x's logistic objective within 1e-2 of the oracle's."""
+    from oracle import scs_ref
+    from paper_1609_03488_b200 import canon
+    A, y, _ = canon.gen_logreg(60, 10, seed=3)
+    lam = 0.05
+    prob = canon.build_logreg(canon.LogRegProblem(A, y, lam))
+    st = scs.ScsSettings(eps=1e-3, max_iters=20000)
+    sol = scs.solve(prob, st)
+    osol, _ = scs_ref.scs_solve(_oracle_problem(prob),
+                                scs_ref.ScsOracleSettings(eps=1e-3, max_iters=20000))
+    assert sol.status == osol.status
+    assert abs(sol.iterations - osol.iterations) <= max(0.05 * osol.iterations, 40)
+    fd = canon.logreg_objective(A, y, lam, sol.x[:10])
+    fo = canon.logreg_objective(A, y, lam, osol.x[:10])
+    assert abs(fd - fo) <= 1e-2 * abs(fo)
+
+
+def test_soc_constrained_ls_end_to_end():
+    """configs[4] (SOC-constrained least squares) at small scale vs oracle."""
+    from oracle import scs_ref
+    from paper_1609_03488_b200 import canon
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((80, 20))
+    b = rng.standard_normal(80)
+    prob = canon.build_soc_ls(canon.SocLsProblem(linop.dense(A), b, 0.5))
+    st = scs.ScsSettings(eps=1e-4, max_iters=50000)
+    sol = scs.solve(prob, st)
+    osol, _ = scs_ref.scs_solve(_oracle_problem(prob),
+                                scs_ref.ScsOracleSettings(eps=1e-4, max_iters=50000))
+    assert sol.status == osol.status == "solved"
+    assert abs(sol.iterations - osol.iterations) <= max(0.02 * osol.iterations, 20)
+    assert abs(sol.pobj - osol.pobj) <= 1e-3 * abs(osol.pobj)
+    assert np.linalg.norm(sol.x[:20]) <= 0.5 * (1 + 1e-3)
