@@ -385,6 +385,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def aggregate(total_s: float, total_iters: int, device=None) -> tuple[float, int]:
+    """Whole-job numbers over the ranks of the default process group: the
+    time is the max over ranks (per-rank device time), the work is summed."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return total_s, total_iters
+    t = torch.tensor([float(total_s)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    it = torch.tensor([float(total_iters)], dtype=torch.float64, device=device)
+    dist.all_reduce(it)
+    return float(t.item()), int(it.item())
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -557,15 +571,7 @@ def run_b200(args) -> None:
     iters = [r[2] for r in results]
     cgs = [r[3] for r in results]
     statuses = {r[4] for r in results}
-    total_s = sum(step_s)
-    total_iters = sum(iters)
-    if world > 1:
-        t = torch.tensor([total_s], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_s = float(t.item())
-        it = torch.tensor([float(total_iters)], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(it)
-        total_iters = int(it.item())
+    total_s, total_iters = aggregate(sum(step_s), sum(iters), "cuda")
     value = total_iters / total_s
 
     # roofline of the dominant kernel (k_scs: the splitting loop)
@@ -610,15 +616,8 @@ def run_b200(args) -> None:
             pobj = sol.pobj
             if step >= 1:
                 e2e_times.append((dt, sol.iterations))
-        e2e_s = sum(t for t, _ in e2e_times)
-        e2e_it = sum(i for _, i in e2e_times)
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t.item())
-            it = torch.tensor([float(e2e_it)], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(it)
-            e2e_it = int(it.item())
+        e2e_s, e2e_it = aggregate(sum(t for t, _ in e2e_times),
+                                  sum(i for _, i in e2e_times), "cuda")
         e2e = {"value": e2e_it / e2e_s, "unit": "iter/s", "h2d_bytes_per_step": wl.h2d_bytes(),
                "d2h_bytes_per_step": d2h, "time_to_eps_s": e2e_s / len(e2e_times),
                "status": e2e_status, "pobj": pobj}
