@@ -1335,14 +1335,23 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
         period = ow;
         kw2max = std::max<int64_t>(kw2max, LF.k1);
       }
+      bool has_dense = false;
+      for (int t = R.term_begin; t < R.term_end; ++t)
+        has_dense |= d->leaves[d->terms[t].leaf].kind == CGB_LEAF_DENSE;
+      D.rpt = 32 * D.rfac;
+      D.pad = 0;
       if (period > 0 && periodic_ok) {
         D.rfac = CGB_RC;
+        D.rpt = 32 * CGB_RC;
         D.period = period;
         D.tpr = (int32_t)((period + 32 * CGB_RC - 1) / (32 * CGB_RC));
         tiles += (R.row_end - R.row_begin) / period * D.tpr;
       } else {
-        const int64_t rows_per_tile = 32 * (int64_t)D.rfac;
-        tiles += (R.row_end - R.row_begin + rows_per_tile - 1) / rows_per_tile;
+        // dense (GEMV) blocks: a warp per 8 rows, so short-wide matrices
+        // spread over many warps (the rows' loads of a tile are in flight
+        // together; see leaf_tile)
+        if (has_dense && D.rfac == 1) D.rpt = 8;
+        tiles += (R.row_end - R.row_begin + D.rpt - 1) / D.rpt;
       }
       ++idx;
     }

@@ -40,12 +40,14 @@ struct DevRowBlock {
   int32_t rfac;       // rows per lane in this block's tiles (1 or CGB_RC)
   int32_t conv_term;  // the block's only 1-d conv term (TMA-staged), or -1
   int32_t tpr;        // periodic blocks: tiles per row
+  int32_t rpt;        // rows per tile (32 * rfac, or fewer for dense blocks)
+  int32_t pad;
 };
 
 // first row and row count of a tile of row block rb
 __device__ __forceinline__ void tile_rows(const DevRowBlock& rb, int64_t tile, int64_t& row0,
                                           int& nvalid) {
-  const int64_t rpt = 32 * (int64_t)rb.rfac;
+  const int64_t rpt = rb.rpt;
   const int64_t t = tile - rb.tile_begin;
   if (rb.period > 0) {
     const int64_t pr = t / rb.tpr, pc = t - pr * rb.tpr;
@@ -610,7 +612,7 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
           const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
           rowp[q] = L.val + (lrow0 + rr) * L.ld;
         }
-#pragma unroll 2
+#pragma unroll 4
         for (int64_t c = lane; c < cols; c += 32) {
           const double xv = in(c);
 #pragma unroll

@@ -30,11 +30,19 @@ t2 = time.time()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 plan.reset()
 plan.run(5)
+prof = "--profile" in sys.argv
+if prof:
+    plan.enable_profile(True)
 e0.record()
 plan.run(iters)
 e1.record()
 torch.cuda.synchronize()
 st = plan.state()
+if prof:
+    ph = plan.profile()
+    print(json.dumps({k: (1e6 * v / iters if not isinstance(v, dict) else v)
+                      for k, v in ph.items()}))
+    plan.enable_profile(False)
 out = {"workload": wl.name, "data_s": t1 - t0, "build_s": t2 - t1,
        "setup_cg_iters": plan.cached.setup_cg_iters,
        "us_per_iter": 1e3 * e0.elapsed_time(e1) / iters, "cg_per_iter": float(st[_lib.ST_CGT]) / max(1, st[_lib.ST_K])}
