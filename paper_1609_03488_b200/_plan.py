@@ -191,8 +191,47 @@ class _Builder:
         rows = e.cols if adj else e.rows
         if rows == 0 or (e.rows if adj else e.cols) == 0:
             return
+        if isinstance(e, L.DenseMatrix) and self._emit_split_dense(e, adj, in_buf, in_off,
+                                                                   out_buf, out_row, alpha, level):
+            return
         li = self.leaf(e, adj)
         self.terms.append((li, in_buf, out_row, in_off, float(alpha), out_buf))
+
+    # short-wide GEMV (e.g. A^T of a tall A): a warp per row block would put
+    # a handful of warps on the whole matrix, so the columns are split into
+    # P slices whose partial products land in a temporary one level deeper,
+    # summed by P identity terms -- a deterministic split-K.
+    SPLIT_MIN_COLS = 8192
+
+    def _emit_split_dense(self, e, adj, in_buf, in_off, out_buf, out_row, alpha, level) -> bool:
+        base, badj = (e._transpose_of, not adj) if e._transpose_of is not None else (e, adj)
+        rows, cols = (base.cols, base.rows) if badj else (base.rows, base.cols)
+        if cols < self.SPLIT_MIN_COLS or cols < 16 * rows:
+            return False
+        nsplit = int(min(32, -(-cols // 4096)))
+        chunk = -(-cols // nsplit)
+        nsplit = -(-cols // chunk)
+        t = self.new_temp(nsplit * rows, level + 1)
+        for k in range(nsplit):
+            c0 = k * chunk
+            cw = min(chunk, cols - c0)
+
+            def make(c0=c0, cw=cw):
+                buf = _leaf_buffers(base)
+                key = "adj" if badj else "fwd"
+                if key not in buf:
+                    buf[key] = _cuda(base.values.T if badj else base.values)
+                tt = buf[key]
+                self.keep.append(tt)
+                return _lib.Leaf(kind=_lib.LEAF_DENSE, rows=rows, cols=cw,
+                                 val=tt.data_ptr() + 8 * c0, ld=cols), 0
+            li = self._add_leaf((id(base), badj, "split", k, nsplit), make)
+            self.terms.append((li, in_buf, k * rows, in_off + c0, 1.0, t))
+        ident = self._add_leaf(("I", rows), lambda: (_lib.Leaf(kind=_lib.LEAF_IDENTITY,
+                                                               rows=rows, cols=rows), 0))
+        for k in range(nsplit):
+            self.terms.append((ident, t, out_row, k * rows, float(alpha), out_buf))
+        return True
 
     def finish(self, in_len: int, out_len: int):
         buf_len = [out_len] + self.temp_len

@@ -420,3 +420,21 @@ def test_soc_constrained_ls_end_to_end():
     assert abs(sol.iterations - osol.iterations) <= max(0.02 * osol.iterations, 20)
     assert abs(sol.pobj - osol.pobj) <= 1e-3 * abs(osol.pobj)
     assert np.linalg.norm(sol.x[:20]) <= 0.5 * (1 + 1e-3)
+
+
+def test_short_wide_dense_split_matches_numpy():
+    """A tall dense A (its adjoint is a short-wide GEMV, lowered as a
+    column-split with a deterministic identity-sum level) and a wide A:
+    forward / adjoint vs numpy, and the adjoint identity."""
+    rng = np.random.default_rng(31)
+    for m, n in [(20000, 300), (150, 30000), (9000, 9000 // 20)]:
+        Ad = rng.standard_normal((m, n))
+        op = linop.dense(Ad)
+        x = rng.standard_normal(n)
+        y = rng.standard_normal(m)
+        np.testing.assert_allclose(op.forward(x), Ad @ x, rtol=1e-11, atol=1e-10)
+        np.testing.assert_allclose(op.adjoint_apply(y), Ad.T @ y, rtol=1e-11, atol=1e-10)
+        cop = linop.scale(-2.0, linop.vstack([op, linop.identity(n)]))
+        yy = rng.standard_normal(m + n)
+        np.testing.assert_allclose(cop.adjoint_apply(yy),
+                                   -2.0 * (Ad.T @ yy[:m] + yy[m:]), rtol=1e-11, atol=1e-9)
