@@ -53,3 +53,60 @@ def test_bench_aggregation_two_ranks():
 def test_aggregate_single_process_is_identity():
     import bench
     assert bench.aggregate(2.5, 7) == (2.5, 7)
+
+
+def _shard_worker(rank, world, port, name, steps, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        import _exprs as E
+        from _golden import build_cones, build_tree, load
+        from oracle import scs_ref, shard_ref
+        data, meta = load(name)
+        prob = E.Problem(build_tree(meta["tree"], data, E), np.array(data["b"]),
+                         np.array(data["c"]), E.ConeProduct(build_cones(meta["cones"], E)))
+        s = scs_ref.ScsOracleSettings(**meta["settings"])
+        comm = shard_ref.TorchComm()
+        st, sh = shard_ref.solve(prob, comm, s, max_steps=steps)
+        out[rank] = (st.ux.tolist(), st.uy.tolist(), st.utau, st.vy.tolist(), st.kappa,
+                     st.k, st.cgt, st.status, (sh.r0, sh.r1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,steps", [("scs_lasso_dense_30_7", 12), ("scs_deconv_100_0", 40),
+                                        ("scs_soc_ball", 30)])
+def test_row_sharded_iteration_matches_single_process(name, steps):
+    """§8e decomposition: the splitting iteration with y-space rows split over
+    2 gloo ranks (A^T y and y-space dots all-reduced, straddling SOC norms
+    reduced) reproduces the single-process oracle's iterates."""
+    import numpy as np
+    import _exprs as E
+    from _golden import build_cones, build_tree, load
+    from oracle import scs_ref
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_shard_worker, args=(world, port, name, steps, out), nprocs=world, join=True)
+        res = dict(out)
+    data, meta = load(name)
+    prob = E.Problem(build_tree(meta["tree"], data, E), np.array(data["b"]),
+                     np.array(data["c"]), E.ConeProduct(build_cones(meta["cones"], E)))
+    s = scs_ref.ScsOracleSettings(**meta["settings"])
+    ref = None
+    for _, st in scs_ref.iterate(prob, s, scs_ref.prepare_subspace(prob, s.setup_cg_tol,
+                                                                   s.cg_max_iter), steps):
+        ref = st
+    n, m = prob.A.cols, prob.A.rows
+    uy = np.concatenate([np.array(res[r][1]) for r in range(world)])
+    vy = np.concatenate([np.array(res[r][3]) for r in range(world)])
+    assert res[0][8][1] == res[1][8][0] and res[1][8][1] == m   # a row partition
+    np.testing.assert_allclose(res[0][0], res[1][0])             # x replicated, identical
+    u = np.concatenate([res[0][0], uy, [res[0][2]]])
+    v = np.concatenate([np.zeros(n), vy, [res[0][4]]])
+    scale = 1.0 + np.linalg.norm(ref.u)
+    assert np.linalg.norm(u - ref.u) <= 1e-8 * scale
+    assert np.linalg.norm(v - ref.v) <= 1e-8 * scale
+    assert res[0][5] == ref.k and res[0][6] == ref.cgt
