@@ -12,7 +12,7 @@ import os
 import threading
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libcgb200.so")
+LIB_PATH = os.environ.get("CGB200_LIB") or os.path.join(LIB_DIR, "libcgb200.so")
 
 ABI_VERSION = 1
 

@@ -390,6 +390,7 @@ struct CgUpdDirect {
 // Runs CG from r = b - apply(x) (stored in B.r) with rns = r.r.  Returns the
 // iteration count.  With tracking (B.c != null) *cx += alpha c.p and
 // *bax += alpha b.t follow c.x and b.(A x) through the updates.
+template <bool TD>
 __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, double lam,
                            const CgBufs& B, int64_t n, int64_t m, double& rns, double delta,
                            double floor_, int64_t max_iter, GridSync& gs, double* cx,
@@ -405,7 +406,7 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
       double s[4] = {0.0, 0.0, 0.0, 0.0};
       {
         EpiT et{B.t, track ? B.b : nullptr, beta, first};
-        apply_plan(F, rin, et, s, gs);
+        apply_plan<TD>(F, rin, et, s, gs);
         double pp = 0.0, cp = 0.0;
         if (first) {
           if (track) pdots<false, true>(n, B.r, B.p, B.c, beta, pp, cp);
@@ -428,7 +429,7 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
       {
         const InVec tin{B.t, nullptr, 0.0};
         EpiCgUpd eu{B.r, B.p, B.x, B.gx, beta, first, lam, alpha};
-        apply_plan(Aj, tin, eu, rr, gs);
+        apply_plan<TD>(Aj, tin, eu, rr, gs);
         if (B.ax) {
           AxUpd f{B.ax, alpha};
           const double* src[2] = {B.ax, B.t};
@@ -442,7 +443,7 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
     } else {
       double pq[1] = {0.0};
       EpiQDirect eq{pin, B.q, beta, first};
-      apply_plan(F, rin, eq, pq, gs);
+      apply_plan<TD>(F, rin, eq, pq, gs);
       gs.reduce(pq);
       prof.mark(PROF_CG_F);
       const double alpha = rns / pq[0];
@@ -475,13 +476,14 @@ struct ApplyArgs {
   const double* x; double* y;
 };
 
+template <bool TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) {
   tma_init();
   const DevPlan& P = *cache_plan(0, a.P);
   GridSync gs(a.bar, a.partials);
   InVec in{a.x, nullptr, 0.0};
   EpiStore st{a.y};
-  apply_plan(P, in, st, nullptr, gs);
+  apply_plan<TD>(P, in, st, nullptr, gs);
 }
 
 struct ConeArgs {
@@ -524,6 +526,7 @@ struct CgArgs {
   double* result;  // [iterations, rns, bnorm2]
 };
 
+template <bool TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) {
   tma_init();
   const DevPlan& F = *cache_plan(0, a.F);
@@ -534,21 +537,21 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constan
   InVec xin{a.x, nullptr, 0.0};
   if (a.recipe == CGB_RECIPE_NORMAL) {
     EpiStore st{a.t};
-    apply_plan(F, xin, st, nullptr, gs);
+    apply_plan<TD>(F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.t, nullptr, 0.0};
     EpiR0 e{a.b, a.x, a.r, a.lam, 1};
-    apply_plan(Aj, tin, e, s, gs);
+    apply_plan<TD>(Aj, tin, e, s, gs);
   } else {
     EpiR0 e{a.b, a.x, a.r, 0.0, 0};
-    apply_plan(F, xin, e, s, gs);
+    apply_plan<TD>(F, xin, e, s, gs);
   }
   gs.reduce(s);
   double rns = s[0];
   const double delta = a.tol * sqrt(s[1]);
   const double floor_ = a.eps_floor * s[1];
   CgBufs B{a.x, a.r, a.p, a.q, a.t, nullptr, nullptr, nullptr, nullptr};
-  const int64_t k = cg_loop(F, Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
+  const int64_t k = cg_loop<TD>(F, Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.result[0] = (double)k;
@@ -584,6 +587,7 @@ __device__ __forceinline__ double side_dot(int64_t n, const double* x, const dou
 
 // Inner block solve, the reference's arithmetic (scs.py:170-187):
 // rhs = d1 - A^T d2 ; r0 = rhs - (x0 + A^T A x0) ; CG ; z2 = d2 + A z1.
+template <bool TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) {
   tma_init();
   const DevPlan& F = *cache_plan(0, a.F);
@@ -596,31 +600,31 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_cons
   {
     InVec xin{z1, nullptr, 0.0};
     EpiStore st{a.tx};
-    apply_plan(F, xin, st, nullptr, gs);
+    apply_plan<TD>(F, xin, st, nullptr, gs);
     gs.sync();
     InVec tin{a.tx, nullptr, 0.0};
     EpiStore st2{a.gx};
-    apply_plan(Aj, tin, st2, nullptr, gs);
+    apply_plan<TD>(Aj, tin, st2, nullptr, gs);
     gs.sync();
   }
   double s[3] = {0.0, 0.0, 0.0};
   {
     InVec din{a.d2, nullptr, 0.0};
     EpiRhs e{a.d1, z1, a.gx, nullptr, a.r, nullptr, 0.0};
-    apply_plan(Aj, din, e, s, gs);
+    apply_plan<TD>(Aj, din, e, s, gs);
     gs.reduce(s);
   }
   double rns = s[1];
   const double delta = a.tol * sqrt(s[0]);
   const double floor_ = a.eps_floor * s[0];
   CgBufs B{z1, a.r, a.p, nullptr, a.t, nullptr, nullptr, nullptr, nullptr};
-  const int64_t k = cg_loop(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
+  const int64_t k = cg_loop<TD>(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   double h[2] = {0.0, 0.0};
   {
     InVec xin{z1, nullptr, 0.0};
     EpiZ2 e{nullptr, z2, a.d2, a.b};
-    apply_plan(F, xin, e, h, gs);
+    apply_plan<TD>(F, xin, e, h, gs);
     if (a.c) {
       h[1] = side_dot(a.n, a.c, z1);
     }
@@ -757,6 +761,7 @@ struct SocPassB2 {
   }
 };
 
+template <bool TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
   tma_init();
@@ -816,7 +821,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
       InVec in{wy, nullptr, 0.0};
       EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev};
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = a.prof + 16;
-      apply_plan(Aj, in, e, s, gs);
+      apply_plan<TD>(Aj, in, e, s, gs);
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = nullptr;
       gs.reduce(s);
     }
@@ -828,7 +833,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double cx = s[2];
     const double bwy = s[3];
     CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c};
-    const int64_t cgk = cg_loop(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
+    const int64_t cgk = cg_loop<TD>(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
                                 cg_max, gs, &cx, &bax, prof);
     // tau~ = (w_tau + h.p) / (1 + h.g) with h.p = c.p1 + b.(w_y + A p1)
     const double tau_t = (wtau + (cx + (bwy + bax))) / a.denom;
@@ -981,7 +986,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
       InVec uyin{W.u + n, nullptr, 0.0};
       EpiRawP ep{W.v + n, a.b, utau};
       EpiRawD ed{a.c, utau};
-      apply_two(F, uxin, ep, Aj, uyin, ed, q, gs);
+      apply_two<TD>(F, uxin, ep, Aj, uyin, ed, q, gs);
       q[4] = side_dot(n, a.c, W.u);
       q[5] = side_dot(m, a.b, W.u + n);
       gs.reduce(q);
@@ -1503,7 +1508,7 @@ int cgb_ctx_destroy(cgb_ctx* ctx) {
 int cgb_ctx_geometry(const cgb_ctx* ctx, int32_t* out3) {
   if (!ctx || !out3) return fail(CGB_EINVAL, "null argument");
   int grid = 0;
-  int rc = grid_for(ctx, k_scs, 0, &grid);
+  int rc = grid_for(ctx, k_scs<false>, 0, &grid);
   if (rc) return rc;
   out3[0] = ctx->num_sms;
   out3[1] = grid / ctx->num_sms;
@@ -1542,7 +1547,8 @@ int cgb_op_apply(cgb_ctx* ctx, const cgb_op* op, int adjoint, const double* x, d
                  void* stream) {
   if (!ctx || !op || !x || !y) return fail(CGB_EINVAL, "null argument");
   ApplyArgs a{ctx->bar, ctx->partials, adjoint ? op->adj.dp : op->fwd.dp, x, y};
-  return launch_coop(ctx, k_apply, a, plan_smem(a.P), (cudaStream_t)stream);
+  if (a.P.smem_xs2 > 0) return launch_coop(ctx, k_apply<true>, a, plan_smem(a.P), (cudaStream_t)stream);
+  return launch_coop(ctx, k_apply<false>, a, plan_smem(a.P), (cudaStream_t)stream);
 }
 
 int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, int32_t ncones,
@@ -1639,7 +1645,9 @@ int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const d
   CgArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, recipe, lam, b, x,
            scratch, scratch + n, scratch + 2 * n, scratch + 3 * n,
            n, m, tol, max_iter, eps_floor_for(n), ctx->result};
-  int rc = launch_coop(ctx, k_cg, a, solver_smem(a.F, a.Aj), s);
+  int rc = (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
+               ? launch_coop(ctx, k_cg<true>, a, solver_smem(a.F, a.Aj), s)
+               : launch_coop(ctx, k_cg<false>, a, solver_smem(a.F, a.Aj), s);
   if (rc == CGB_OK) {
     CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 3 * sizeof(double),
                              cudaMemcpyDeviceToHost, s));
@@ -1664,7 +1672,9 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
   InnerArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, d1, d2, z, c, b,
               scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, scratch + 3 * n + m,
               n, m, tol, max_iter, eps_floor_for(n), ctx->result};
-  int rc = launch_coop(ctx, k_inner, a, solver_smem(a.F, a.Aj), s);
+  int rc = (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
+               ? launch_coop(ctx, k_inner<true>, a, solver_smem(a.F, a.Aj), s)
+               : launch_coop(ctx, k_inner<false>, a, solver_smem(a.F, a.Aj), s);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 4 * sizeof(double),
                            cudaMemcpyDeviceToHost, s));
@@ -1727,7 +1737,9 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   size_t smem = base;
   if (sizeof(double) * (size_t)need <= kMaxSmem) smem = std::max(smem, sizeof(double) * (size_t)need);
   a.stash_cap = (int)(smem / sizeof(double));
-  return launch_coop(ctx, k_scs, a, smem, (cudaStream_t)stream);
+  if (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
+    return launch_coop(ctx, k_scs<true>, a, smem, (cudaStream_t)stream);
+  return launch_coop(ctx, k_scs<false>, a, smem, (cudaStream_t)stream);
 }
 
 int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc) {

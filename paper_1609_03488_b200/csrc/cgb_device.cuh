@@ -45,11 +45,12 @@ struct DevRowBlock {
 };
 
 // first row and row count of a tile of row block rb
+template <bool PERIODIC>
 __device__ __forceinline__ void tile_rows(const DevRowBlock& rb, int64_t tile, int64_t& row0,
                                           int& nvalid) {
   const int64_t rpt = rb.rpt;
   const int64_t t = tile - rb.tile_begin;
-  if (rb.period > 0) {
+  if (PERIODIC && rb.period > 0) {
     const int64_t pr = t / rb.tpr, pc = t - pr * rb.tpr;
     row0 = rb.row_begin + pr * rb.period + pc * rpt;
     const int64_t rem = rb.period - pc * rpt;
@@ -578,6 +579,7 @@ __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0, int n
 // 1-d convolution / correlation leaves in R == CGB_RC tiles run the
 // register-blocked path (conv_compute) on a window staged in shared memory:
 // by TMA in run_level for interior tiles, by hand (zero-filled edges) here.
+template <bool WITH2D>
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
                                           double (&acc)[CGB_RC], int lane, const double* cc,
@@ -692,7 +694,10 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
     } break;
     case CGB_LEAF_CONV2D:
     case CGB_LEAF_CORR2D: {
-      if (R == CGB_RC && cc && ring) {
+      // the tiled 2-d path (a call) exists only in the WITH2D kernels, which
+      // the host launches for plans with a 2-d leaf: it cost every other
+      // plan ~10 % (register allocation around the call) when always present
+      if (WITH2D && R == CGB_RC && cc && ring) {
         conv2d_tile(L, lrow0, nvalid, in.a, alpha, cc, ring, xs2, os, acc, lane);
         break;
       }
@@ -796,7 +801,7 @@ __device__ __forceinline__ void issue_window(const ConvWin& w, double* dst, uint
 // epi.tile(first_row, tile_row0, R, left, acc, part) with rows first_row + 32 r,
 // valid while 32 r < left (see CGB_EPI_VALID) -- so it can issue all its
 // loads before its stores.
-template <class Epi>
+template <bool WITH2D, class Epi>
 __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
                           double* part) {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
@@ -822,7 +827,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
   if (tile < T) {
     rbi = find_rowblock(P, rb_lo, rb_hi, tile);
     const DevRowBlock& rb = P.rbs[rbi];
-    tile_rows(rb, tile, row0, nvalid);
+    tile_rows<WITH2D>(rb, tile, row0, nvalid);
     win = conv_window(P, rb, row0, in, temp);
     if (win.ok) issue_window(win, xsb0, &bar[0], lane);
   }
@@ -841,7 +846,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
     if (ntile < T) {
       nrbi = find_rowblock(P, rb_lo, rb_hi, ntile);
       const DevRowBlock& nrb = P.rbs[nrbi];
-      tile_rows(nrb, ntile, nrow0, nnvalid);
+      tile_rows<WITH2D>(nrb, ntile, nrow0, nnvalid);
       nwin = conv_window(P, nrb, nrow0, in, temp);
       if (nwin.ok) issue_window(nwin, cur ? xsb0 : xsb1, &bar[cur ^ 1], lane);
     }
@@ -867,7 +872,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       const InVec tin = tm.in_buf == 0
                             ? in.shift(tm.in_off)
                             : InVec{temp + P.temp_off[tm.in_buf - 1] + tm.in_off, nullptr, 0.0};
-      leaf_tile(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os,
+      leaf_tile<WITH2D>(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os,
                 tin.b ? nullptr : ring, P.smem_xs2);
     }
     if (tl) { const uint64_t x = globaltimer(); tl[3] += (double)(x - tl1); tl1 = x; }
@@ -899,27 +904,27 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
 
 // Full application; levels separated by grid barriers.  No barrier after the
 // final level: the caller follows with a reduction or sync.
-template <class Epi>
+template <bool WITH2D, class Epi>
 __device__ void apply_plan(const DevPlan& P, const InVec& in, Epi& epi, double* part,
                            GridSync& gs, int ts = 0) {
   for (int e = 0; e < P.nlevels; ++e) {
     if (e) gs.sync();
-    run_level(P, e, in, ts, epi, part);
+    run_level<WITH2D>(P, e, in, ts, epi, part);
   }
 }
 
 // Two independent applications in one phase (levels aligned at the end);
 // the second uses temporary set 1, so both may be the same plan.
-template <class E1, class E2>
+template <bool WITH2D, class E1, class E2>
 __device__ void apply_two(const DevPlan& P1, const InVec& in1, E1& e1, const DevPlan& P2,
                           const InVec& in2, E2& e2, double* part, GridSync& gs) {
   const int L = P1.nlevels > P2.nlevels ? P1.nlevels : P2.nlevels;
   for (int s = 0; s < L; ++s) {
     if (s) gs.sync();
     const int a = s - (L - P1.nlevels);
-    if (a >= 0) run_level(P1, a, in1, 0, e1, part);
+    if (a >= 0) run_level<WITH2D>(P1, a, in1, 0, e1, part);
     const int b = s - (L - P2.nlevels);
-    if (b >= 0) run_level(P2, b, in2, 1, e2, part);
+    if (b >= 0) run_level<WITH2D>(P2, b, in2, 1, e2, part);
   }
 }
 
