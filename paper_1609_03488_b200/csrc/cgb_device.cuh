@@ -24,6 +24,12 @@
 #ifndef CGB_RC
 #define CGB_RC 9             // rows per lane in convolution tiles (odd: no bank conflicts)
 #endif
+#ifndef CGB_DENSE_DR
+#define CGB_DENSE_DR 8       // dense GEMV: rows per warp-group (loads in flight together)
+#endif
+#ifndef CGB_DENSE_UNROLL
+#define CGB_DENSE_UNROLL 4   // dense GEMV: column chunks unrolled per row group
+#endif
 #define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
 #define CGB_U 8              // elements per thread per batch in streaming loops
 
@@ -600,7 +606,8 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
     case CGB_LEAF_DENSE: {
       // warp per row, CGB_DR rows at a time so their loads are in flight
       // together (one latency per row group instead of per row)
-      constexpr int CGB_DR = 8;
+      constexpr int CGB_DR = CGB_DENSE_DR;
+      constexpr int CGB_DU = CGB_DENSE_UNROLL;
       double mine[CGB_RC];
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
@@ -614,7 +621,7 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
           const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
           rowp[q] = L.val + (lrow0 + rr) * L.ld;
         }
-#pragma unroll 4
+#pragma unroll CGB_DU
         for (int64_t c = lane; c < cols; c += 32) {
           const double xv = in(c);
 #pragma unroll
