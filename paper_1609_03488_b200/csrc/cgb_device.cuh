@@ -964,15 +964,11 @@ struct SocCoef {
 };
 
 // Exponential cone K_exp = cl{(x,y,z): y > 0, y e^{x/y} <= z}: projection of
-// one 3-vector, the same algorithm as oracle/expcone_ref.py (stationarity in
+// one 3-vector, the algorithm of oracle/expcone_ref.py (stationarity in
 // rho = x/y, roots of the e^{-2rho}-scaled equation G bracketed on a unit
-// grid over [-60, 40] and bisected; the root with s_p > 0, mu >= 0 or the
-// face point y = 0, whichever is closer).  A thread per cone.
-__device__ __forceinline__ double exp_g(double rho, double r, double s, double t) {
-  const double e1 = exp(-rho);
-  return (r - s * rho) * e1 * e1 + (r - r * rho - s) + t * e1 * (rho * rho - rho + 1.0);
-}
-
+// grid over [-60, 40]; the root with s_p > 0, mu >= 0 or the face point
+// y = 0, whichever is closer), with the roots polished by safeguarded Newton
+// instead of bisection.  A thread per cone.
 __device__ void exp_project(double& r, double& s, double& t) {
   // 1. inside K_exp
   if (s > 0.0) {
@@ -996,26 +992,53 @@ __device__ void exp_project(double& r, double& s, double& t) {
     t = fmax(t, 0.0);
     return;
   }
-  // 4. curved boundary (or the face)
+  // 4. curved boundary (or the face).  Brackets from a unit-step scan of G
+  //    with e^{-rho} carried multiplicatively (no exp in the scan); then
+  //    every lane polishes its k-th bracket by safeguarded Newton at the same
+  //    time (polishing inside the scan serialised a warp's lanes).
   double br = fmin(r, 0.0), bs = 0.0, bt = fmax(t, 0.0);
   double bd = (r - br) * (r - br) + s * s + (t - bt) * (t - bt);
-  double lo = -60.0, glo = exp_g(lo, r, s, t);
-  while (lo < 40.0) {
+  const double kEm1 = 0.36787944117144233;  // e^{-1}
+  constexpr int kMaxBr = 3;
+  double blo[kMaxBr];
+  bool bneg[kMaxBr];
+  int nb = 0;
+  double lo = -60.0;
+  double e1 = exp(60.0);                     // e^{-lo}
+  double glo = (r - s * lo) * e1 * e1 + (r - r * lo - s) + t * e1 * (lo * lo - lo + 1.0);
+  for (int step = 0; step < 100; ++step) {
     const double hi = lo + 1.0;
-    const double ghi = exp_g(hi, r, s, t);
-    if ((glo < 0.0) != (ghi < 0.0) || ghi == 0.0) {
-      double a = lo, b = hi, ga = glo;
-      for (int it = 0; it < 64; ++it) {
-        const double mid = 0.5 * (a + b);
-        const double gm = exp_g(mid, r, s, t);
-        if ((gm < 0.0) == (ga < 0.0)) {
-          a = mid;
-          ga = gm;
-        } else {
-          b = mid;
-        }
+    const double e1h = e1 * kEm1;
+    const double ghi = (r - s * hi) * e1h * e1h + (r - r * hi - s) + t * e1h * (hi * hi - hi + 1.0);
+    if (((glo < 0.0) != (ghi < 0.0) || ghi == 0.0) && nb < kMaxBr) {
+      blo[nb] = lo;
+      bneg[nb] = glo < 0.0;
+      ++nb;
+    }
+    lo = hi;
+    e1 = e1h;
+    glo = ghi;
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxBr; ++j) {
+    if (j < nb) {
+      double a = blo[j], b = blo[j] + 1.0;
+      const bool alo_neg = bneg[j];
+      double x = 0.5 * (a + b);
+      for (int it = 0; it < 40; ++it) {
+        const double ex = exp(-x);
+        const double g = (r - s * x) * ex * ex + (r - r * x - s) + t * ex * (x * x - x + 1.0);
+        if (g == 0.0) break;
+        if ((g < 0.0) == alo_neg) a = x; else b = x;
+        const double dg = (-s - 2.0 * (r - s * x)) * ex * ex - r + t * ex * (-x * x + 3.0 * x - 2.0);
+        double xn = x - g / dg;
+        if (!(xn > a && xn < b)) xn = 0.5 * (a + b);   // safeguard: bisect
+        const double stp = fabs(xn - x);
+        x = xn;
+        // quadratic convergence: a step of 1e-9 leaves ~1e-18 of error
+        if (stp <= 1e-9 * (1.0 + fabs(x)) || b - a <= 4e-16 * (1.0 + fabs(x))) break;
       }
-      const double rho = 0.5 * (a + b);
+      const double rho = x;
       const double e = exp(rho);
       const double sp = (r * rho + s + t * e) / (rho * rho + 1.0 + e * e);
       const double mu = sp * e - t;
@@ -1030,8 +1053,6 @@ __device__ void exp_project(double& r, double& s, double& t) {
         }
       }
     }
-    lo = hi;
-    glo = ghi;
   }
   r = br;
   s = bs;
