@@ -648,7 +648,20 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
           const int64_t lrow = lrow0 + lane + 32 * r;
           double s = 0.0;
           const int64_t e0 = __ldg(L.rowptr + lrow), e1 = __ldg(L.rowptr + lrow + 1);
-          for (int64_t e = e0; e < e1; ++e) s += __ldg(L.val + e) * in(__ldg(L.colidx + e));
+          int64_t e = e0;
+          // batches of 8 nonzeros: all index / value loads, then all gathers
+          for (; e + 8 <= e1; e += 8) {
+            int32_t ci[8];
+            double vv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              ci[q] = __ldg(L.colidx + e + q);
+              vv[q] = __ldg(L.val + e + q);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += vv[q] * in(ci[q]);
+          }
+          for (; e < e1; ++e) s += __ldg(L.val + e) * in(__ldg(L.colidx + e));
           acc[r] += alpha * s;
         }
       }
