@@ -52,6 +52,57 @@ def _leaf_buffers(e) -> dict:
     return cache
 
 
+def _perm(rows_of_cols: np.ndarray) -> "L.SparseMatrix":
+    """Permutation matrix P with P[rows_of_cols[c], c] = 1."""
+    import scipy.sparse
+    k = len(rows_of_cols)
+    return L.SparseMatrix(scipy.sparse.csc_matrix(
+        (np.ones(k), (rows_of_cols, np.arange(k))), shape=(k, k)))
+
+
+def _block_diag(e, copies: int):
+    """I_copies (x) e as an expression (zero blocks lower to nothing)."""
+    r, c = e.rows, e.cols
+    blocks = []
+    for j in range(copies):
+        parts = []
+        if j:
+            parts.append(L.ZeroOp(r, j * c))
+        parts.append(e)
+        if copies - 1 - j:
+            parts.append(L.ZeroOp(r, (copies - 1 - j) * c))
+        blocks.append(parts[0] if len(parts) == 1 else
+                      L.AdjointOf(L.VStack([L.derive_adjoint(pp) for pp in parts])))
+    return blocks[0] if copies == 1 else L.VStack(blocks)
+
+
+def _kron_tree(e, adj: bool):
+    """Kron(Lk, Rk) (np.kron convention; adjoint = Kron(Lk^T, Rk^T)) as
+    plan-lowerable structure: with x viewed as X (q x s) row-major,
+        T1 = (I_q (x) R) x              Z = X R^T, rows of X
+        T2 = P1 T1                       Z^T (r x q)
+        T3 = (I_r (x) L) T2              (L Z)^T
+        y  = P2 T3                       L Z = L X R^T, row-major (p x r)
+    so the device runs R and L as ordinary leaves and two sparse
+    permutations.  Cached on the expression per direction."""
+    cache = e.__dict__.setdefault("_cgb_kron", {})
+    if adj in cache:
+        return cache[adj]
+    Lk = L.AdjointOf(e.left) if adj else e.left
+    Rk = L.AdjointOf(e.right) if adj else e.right
+    p, q = Lk.rows, Lk.cols
+    r, s = Rk.rows, Rk.cols
+    j = np.repeat(np.arange(q), r)
+    kk = np.tile(np.arange(r), q)
+    p1 = _perm(kk * q + j)                        # T1[j*r + kk] -> T2[kk*q + j]
+    kk2 = np.repeat(np.arange(r), p)
+    i2 = np.tile(np.arange(p), r)
+    p2 = _perm(i2 * r + kk2)                      # T3[kk*p + i] -> y[i*r + kk]
+    tree = L.Compose(p2, L.Compose(_block_diag(Lk, r), L.Compose(p1, _block_diag(Rk, q))))
+    cache[adj] = tree
+    return tree
+
+
 class _Builder:
     def __init__(self):
         self.leaves: list[_lib.Leaf] = []
@@ -187,7 +238,8 @@ class _Builder:
             self.emit(second, adj, t, 0, out_buf, out_row, alpha, level)
             return
         if isinstance(e, L.Kron):
-            raise NotImplementedError("Kron operators are not lowered to device plans yet")
+            self.emit(_kron_tree(e, adj), False, in_buf, in_off, out_buf, out_row, alpha, level)
+            return
         rows = e.cols if adj else e.rows
         if rows == 0 or (e.rows if adj else e.cols) == 0:
             return
