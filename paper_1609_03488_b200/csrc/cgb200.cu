@@ -19,6 +19,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1098,6 +1099,7 @@ struct cgb_ctx {
   double* result;    // small device result buffer
   double* host_result;
   double* prof;      // k_scs phase accumulator (device, PROF_N doubles) or null
+  int grid_override; // CGB_GRID (experiments): fewer CTAs than SMs, 0 = off
 };
 
 struct PlanStore {
@@ -1138,6 +1140,7 @@ int grid_for(const cgb_ctx* ctx, K kernel, size_t smem, int* grid) {
     return fail(CGB_ECOOP, "kernel cannot be resident (threads/registers/shared memory)");
   // one CTA per SM: the persistent kernels size every loop to the grid
   int g = std::min(ctx->num_sms, CGB_MAXG);
+  if (ctx->grid_override > 0) g = std::min(g, ctx->grid_override);
   *grid = g;
   return CGB_OK;
 }
@@ -1480,6 +1483,7 @@ int cgb_ctx_create(int device, cgb_ctx** out) {
   cgb_ctx* c = new cgb_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  if (const char* env = std::getenv("CGB_GRID")) c->grid_override = std::atoi(env);
   c->max_grid = prop.multiProcessorCount * 4;
   if (cudaMalloc(&c->bar, sizeof(GridBar)) != cudaSuccess ||
       cudaMalloc(&c->partials, sizeof(double) * 2 * CGB_MAXP * c->max_grid) != cudaSuccess ||
