@@ -223,7 +223,6 @@ enum ProfPhase : int {
   PROF_CHECK = 7,   // residual check
   PROF_INIT = 8,    // per-launch setup (b.Ax, b.w_y)
   PROF_CONE_AR = 9, // large-SOC pass A reduce alone (profiling only)
-  PROF_CONE_AR2 = 10, // a second, warm reduction of the same size (profiling only)
   PROF_N = 16
 };
 
@@ -934,13 +933,6 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
         gs.reduce(red);
       }
       prof.mark(PROF_CONE_AR);
-      if (a.prof) {  // profiling only: the same reduction again, warm
-        double red2[2 * CGB_MAX_LARGE_SOC];
-#pragma unroll
-        for (int i = 0; i < 2 * CGB_MAX_LARGE_SOC; ++i) red2[i] = 0.0;
-        gs.reduce(red2);
-        prof.mark(PROF_CONE_AR2);
-      }
       // pass B: project the large SOC blocks
       int64_t so = 0;
       for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {

@@ -313,7 +313,7 @@ class SolverPlan:
         return self.buf["state"].cpu().numpy()
 
     PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_x", "cone_elem",
-                      "cone_soc_a", "cone_soc_b", "check", "launch_setup", "cone_soc_a_reduce", "reduce8_warm")
+                      "cone_soc_a", "cone_soc_b", "check", "launch_setup", "cone_soc_a_reduce")
 
     def enable_profile(self, on: bool = True) -> None:
         """Accumulate per-phase device time of later run() calls (ns)."""
