@@ -29,16 +29,38 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
+# translation units compiled in parallel (see the CGB_TU_* flags in cgb200.cu)
+UNITS = ["CGB_TU_HOST", "CGB_TU_SCS0", "CGB_TU_SCS1", "CGB_TU_CG", "CGB_TU_INNER",
+         "CGB_TU_MISC"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", SRC]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(os.path.dirname(OUT), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    procs = []
+    for unit in UNITS:
+        obj = os.path.join(objdir, unit.lower() + ".o")
+        cmd = [nvcc(), *cflags, "-DCGB_SPLIT", f"-D{unit}=1", "-c", "-o", obj, SRC]
+        procs.append((unit, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                  stderr=subprocess.PIPE, text=True)))
+    objs, logs = [], []
+    for unit, obj, pr in procs:
+        out, err = pr.communicate()
+        logs.append(err)
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {unit} ({pr.returncode}):\n{err[-4000:]}")
+        objs.append(obj)
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler",
+            "-fPIC", "-o", OUT + ".tmp", *objs]
+    proc = subprocess.run(link, capture_output=True, text=True)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
+        raise RuntimeError(f"nvcc link failed ({proc.returncode}):\n{proc.stderr[-4000:]}")
     if verbose:
-        print(proc.stderr)
+        print("\n".join(logs))
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

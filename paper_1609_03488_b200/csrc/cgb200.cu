@@ -26,13 +26,44 @@
 
 #include "cgb_device.cuh"
 
+// Translation units: by default this file defines everything.  The build
+// (build.py) compiles it several times in parallel with -DCGB_SPLIT and one
+// CGB_TU_* flag each -- the host C ABI, and groups of kernel instantiations
+// -- and links the objects into one library.
+#ifndef CGB_SPLIT
+#define CGB_TU_HOST 1
+#define CGB_TU_SCS0 1
+#define CGB_TU_SCS1 1
+#define CGB_TU_CG 1
+#define CGB_TU_INNER 1
+#define CGB_TU_MISC 1
+#endif
+#ifndef CGB_TU_HOST
+#define CGB_TU_HOST 0
+#endif
+#ifndef CGB_TU_SCS0
+#define CGB_TU_SCS0 0
+#endif
+#ifndef CGB_TU_SCS1
+#define CGB_TU_SCS1 0
+#endif
+#ifndef CGB_TU_CG
+#define CGB_TU_CG 0
+#endif
+#ifndef CGB_TU_INNER
+#define CGB_TU_INNER 0
+#endif
+#ifndef CGB_TU_MISC
+#define CGB_TU_MISC 0
+#endif
+
 using namespace cgb;
 
 // ===========================================================================
 // epilogues: called once per lane tile (rows first + 32 r, r < R, valid
 // while 32 r < left); all loads are issued before any store.
 // ===========================================================================
-namespace {
+namespace cgbk {
 
 struct EpiStore {  // y -> out
   double* out;
@@ -477,7 +508,9 @@ struct ApplyArgs {
 };
 
 template <bool TD>
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) 
+#if CGB_TU_MISC
+{
   tma_init();
   const DevPlan& P = *cache_plan(0, a.P);
   GridSync gs(a.bar, a.partials);
@@ -485,6 +518,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_cons
   EpiStore st{a.y};
   apply_plan<TD>(P, in, st, nullptr, gs);
 }
+#else
+;
+#endif
 
 struct ConeArgs {
   GridBar* bar; double* partials;
@@ -502,7 +538,9 @@ struct DstVec {
   __device__ void operator()(int64_t i, double x) const { out[i] = x; }
 };
 
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cones(const __grid_constant__ ConeArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cones(const __grid_constant__ ConeArgs a) 
+#if CGB_TU_MISC
+{
   GridSync gs(a.bar, a.partials);
   SrcVec src{a.v};
   DstVec dst{a.out};
@@ -515,6 +553,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cones(const __grid_cons
   }
   cone_project(a.K, a.dual, src, dst, red);
 }
+#else
+;
+#endif
 
 struct CgArgs {
   GridBar* bar; double* partials;
@@ -527,7 +568,9 @@ struct CgArgs {
 };
 
 template <bool TD>
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) 
+#if CGB_TU_CG
+{
   tma_init();
   const DevPlan& F = *cache_plan(0, a.F);
   const DevPlan& Aj = *cache_plan(1, a.Aj);
@@ -559,6 +602,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constan
     a.result[2] = s[1];
   }
 }
+#else
+;
+#endif
 
 struct InnerArgs {
   GridBar* bar; double* partials;
@@ -588,7 +634,9 @@ __device__ __forceinline__ double side_dot(int64_t n, const double* x, const dou
 // Inner block solve, the reference's arithmetic (scs.py:170-187):
 // rhs = d1 - A^T d2 ; r0 = rhs - (x0 + A^T A x0) ; CG ; z2 = d2 + A z1.
 template <bool TD>
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) 
+#if CGB_TU_INNER
+{
   tma_init();
   const DevPlan& F = *cache_plan(0, a.F);
   const DevPlan& Aj = *cache_plan(1, a.Aj);
@@ -637,6 +685,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_cons
     a.result[3] = h[1] + h[0];
   }
 }
+#else
+;
+#endif
 
 // ---------------------------------------------------------------------------
 // the splitting solver
@@ -657,7 +708,7 @@ struct ScsArgs {
 };
 
 // CG tolerance exactly as the solver graph computes it (scs.py:290-311)
-__device__ double cg_tolerance_graph(double k, const cgb_scs_settings& s) {
+static __device__ double cg_tolerance_graph(double k, const cgb_scs_settings& s) {
   const double kp1 = k + 1.0;
   const double pw = s.cg_tol_power;
   double den;
@@ -762,7 +813,9 @@ struct SocPassB2 {
 };
 
 template <bool TD>
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) 
+#if CGB_TU_SCS0 || CGB_TU_SCS1
+{
   extern __shared__ __align__(16) double cgb_dyn_smem[];
   tma_init();
   GridSync gs(a.bar, a.partials);
@@ -1025,6 +1078,9 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     state[CGB_ST_LASTCG] = lastcg;
   }
 }
+#else
+;
+#endif
 
 struct BarArgs {
   GridBar* bar; double* partials;
@@ -1032,7 +1088,9 @@ struct BarArgs {
 };
 
 // diagnostics: cost of the grid barrier / grid reduction
-__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_constant__ BarArgs a) {
+__global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_constant__ BarArgs a) 
+#if CGB_TU_MISC
+{
   GridSync gs(a.bar, a.partials);
   double acc = 0.0;
   for (int64_t i = 0; i < a.iters; ++i) {
@@ -1058,8 +1116,35 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_co
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.out[0] = acc;
 }
+#else
+;
+#endif
 
-}  // namespace
+
+// explicit instantiations, one group per translation unit
+#if CGB_TU_SCS0
+template __global__ void k_scs<false>(const __grid_constant__ ScsArgs);
+#endif
+#if CGB_TU_SCS1
+template __global__ void k_scs<true>(const __grid_constant__ ScsArgs);
+#endif
+#if CGB_TU_CG
+template __global__ void k_cg<false>(const __grid_constant__ CgArgs);
+template __global__ void k_cg<true>(const __grid_constant__ CgArgs);
+#endif
+#if CGB_TU_INNER
+template __global__ void k_inner<false>(const __grid_constant__ InnerArgs);
+template __global__ void k_inner<true>(const __grid_constant__ InnerArgs);
+#endif
+#if CGB_TU_MISC
+template __global__ void k_apply<false>(const __grid_constant__ ApplyArgs);
+template __global__ void k_apply<true>(const __grid_constant__ ApplyArgs);
+#endif
+
+}  // namespace cgbk
+using namespace cgbk;
+
+#if CGB_TU_HOST
 
 // ===========================================================================
 // host side
@@ -1745,3 +1830,5 @@ int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc) {
 }
 
 }  // extern "C"
+
+#endif  // CGB_TU_HOST

@@ -516,7 +516,7 @@ __device__ __forceinline__ void stage_row(const double* row, int64_t lo, int64_t
 // taps from the plan) -- conv_accum on a window of the input row.  The kh
 // row windows stream through a per-warp ring of CGB_RING2 shared buffers,
 // TMA bulk copies for interior windows, hand staging at the image edge.
-__device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0, int nvalid,
+static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0, int nvalid,
                                          const double* x, double alpha, const double* taps,
                                          double* ring, int xs2, double* os,
                                          double (&acc)[CGB_RC], int lane) {
@@ -982,7 +982,7 @@ struct SocCoef {
 // grid over [-60, 40]; the root with s_p > 0, mu >= 0 or the face point
 // y = 0, whichever is closer), with the roots polished by safeguarded Newton
 // instead of bisection.  A thread per cone.
-__device__ void exp_project(double& r, double& s, double& t) {
+static __device__ void exp_project(double& r, double& s, double& t) {
   // 1. inside K_exp
   if (s > 0.0) {
     if (r / s < 700.0 && s * exp(r / s) <= t) return;
