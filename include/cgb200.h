@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CGB_ABI_VERSION 1
+#define CGB_ABI_VERSION 2
 
 /* ---- error codes --------------------------------------------------------- */
 #define CGB_OK 0
@@ -161,6 +161,11 @@ typedef struct cgb_scs_problem {
   double denom;        /* 1 + h.g                                            */
   double pr_scale;     /* 1 / (1 + ||b||)                                    */
   double dr_scale;     /* 1 / (1 + ||c||)                                    */
+  /* b (c) is exactly zero outside [b_nz_begin, b_nz_end) ([c_nz_begin,
+   * c_nz_end)): the loop skips those loads.  Both 0 (a zero-initialised
+   * struct) = no information: the whole vector is streamed.               */
+  int64_t b_nz_begin, b_nz_end;
+  int64_t c_nz_begin, c_nz_end;
 } cgb_scs_problem;
 
 /* Device buffers owned by the caller.  N = n + m + 1.

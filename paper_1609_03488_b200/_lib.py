@@ -14,7 +14,7 @@ import threading
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("CGB200_LIB") or os.path.join(LIB_DIR, "libcgb200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # error codes
 CGB_OK = 0
@@ -67,7 +67,9 @@ class ScsSettingsC(ctypes.Structure):
 
 class ScsProblemC(ctypes.Structure):
     _fields_ = [("n", _i64), ("m", _i64), ("A", _vp), ("K", _vp), ("b", _vp), ("c", _vp),
-                ("g", _vp), ("denom", _f64), ("pr_scale", _f64), ("dr_scale", _f64)]
+                ("g", _vp), ("denom", _f64), ("pr_scale", _f64), ("dr_scale", _f64),
+                ("b_nz_begin", _i64), ("b_nz_end", _i64), ("c_nz_begin", _i64),
+                ("c_nz_end", _i64)]
 
 
 class ScsWorkC(ctypes.Structure):

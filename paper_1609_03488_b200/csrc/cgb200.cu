@@ -88,14 +88,16 @@ struct EpiRhs {
   double* r;
   const double* dw;
   double tau_w;
+  int64_t c_lo, c_hi;  // c is zero outside [c_lo, c_hi)
   __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
+    const bool hc = c && jlo < c_hi && jlo + 32 * R > c_lo;  // warp-uniform
     double a[CGB_RC], x[CGB_RC], gg[CGB_RC], cc[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       const int64_t jq = CGB_EPI_IDX(j, q);
       a[q] = dw ? dw[jq] : d1[jq]; x[q] = x0[jq]; gg[q] = g[jq];
-      if (c) cc[q] = c[jq];
+      if (hc) cc[q] = c[jq];
     }
     if (dw) {
 #pragma unroll
@@ -109,7 +111,7 @@ struct EpiRhs {
         r[j + 32 * q] = rr;
         part[0] += rhs * rhs;
         part[1] += rr * rr;
-        if (c) part[2] += cc[q] * x[q];
+        if (hc) part[2] += cc[q] * x[q];
       }
     }
   }
@@ -298,6 +300,8 @@ struct CgBufs {
   double* gx;  // n, tracked A^T A x (or null)
   const double* b;  // m, tracking dots (or null)
   const double* c;  // n, tracking dots (or null)
+  int64_t b_lo, b_hi;  // b is zero outside [b_lo, b_hi)
+  int64_t c_lo, c_hi;  // c is zero outside [c_lo, c_hi)
 };
 
 // phase F (normal): t = A p by linearity, A p = A r + beta A p_old, i.e.
@@ -307,13 +311,15 @@ struct EpiT {
   const double* b;
   double beta;
   int first;
+  int64_t b_lo, b_hi;  // b is zero outside [b_lo, b_hi)
   __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
+    const bool hb = b && jlo < b_hi && jlo + 32 * R > b_lo;  // warp-uniform
     double bb[CGB_RC], to[CGB_RC];
 #pragma unroll
     for (int q = 0; q < CGB_RC; ++q) {
       const int64_t iq = CGB_EPI_IDX(i, q);
-      if (b) bb[q] = b[iq];
+      if (hb) bb[q] = b[iq];
       if (!first) to[q] = t[iq];
     }
 #pragma unroll
@@ -322,7 +328,7 @@ struct EpiT {
         const double tv = first ? y[q] : y[q] + beta * to[q];
         t[i + 32 * q] = tv;
         part[0] += tv * tv;
-        if (b) part[3] += bb[q] * tv;
+        if (hb) part[3] += bb[q] * tv;
       }
     }
   }
@@ -436,15 +442,22 @@ __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, doub
     if (recipe == CGB_RECIPE_NORMAL) {
       double s[4] = {0.0, 0.0, 0.0, 0.0};
       {
-        EpiT et{B.t, track ? B.b : nullptr, beta, first};
+        EpiT et{B.t, track ? B.b : nullptr, beta, first, B.b_lo, B.b_hi};
         apply_plan<TD>(F, rin, et, s, gs);
         double pp = 0.0, cp = 0.0;
+        // a c with few nonzeros (stuffed objectives) is dotted by one thread
+        const bool c_short = track && B.c_hi - B.c_lo <= 64;
+        const bool c_stream = track && !c_short;
         if (first) {
-          if (track) pdots<false, true>(n, B.r, B.p, B.c, beta, pp, cp);
+          if (c_stream) pdots<false, true>(n, B.r, B.p, B.c, beta, pp, cp);
           else pdots<false, false>(n, B.r, B.p, B.c, beta, pp, cp);
         } else {
-          if (track) pdots<true, true>(n, B.r, B.p, B.c, beta, pp, cp);
+          if (c_stream) pdots<true, true>(n, B.r, B.p, B.c, beta, pp, cp);
           else pdots<true, false>(n, B.r, B.p, B.c, beta, pp, cp);
+        }
+        if (c_short && blockIdx.x == 0 && threadIdx.x == 0) {
+          for (int64_t i = B.c_lo; i < B.c_hi; ++i)
+            cp += B.c[i] * (first ? B.r[i] : B.r[i] + beta * B.p[i]);
         }
         s[1] += pp;
         s[2] += cp;
@@ -593,7 +606,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constan
   double rns = s[0];
   const double delta = a.tol * sqrt(s[1]);
   const double floor_ = a.eps_floor * s[1];
-  CgBufs B{a.x, a.r, a.p, a.q, a.t, nullptr, nullptr, nullptr, nullptr};
+  CgBufs B{a.x, a.r, a.p, a.q, a.t, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0};
   const int64_t k = cg_loop<TD>(F, Aj, a.recipe, a.lam, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -658,14 +671,14 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_cons
   double s[3] = {0.0, 0.0, 0.0};
   {
     InVec din{a.d2, nullptr, 0.0};
-    EpiRhs e{a.d1, z1, a.gx, nullptr, a.r, nullptr, 0.0};
+    EpiRhs e{a.d1, z1, a.gx, nullptr, a.r, nullptr, 0.0, 0, 0};
     apply_plan<TD>(Aj, din, e, s, gs);
     gs.reduce(s);
   }
   double rns = s[1];
   const double delta = a.tol * sqrt(s[0]);
   const double floor_ = a.eps_floor * s[0];
-  CgBufs B{z1, a.r, a.p, nullptr, a.t, nullptr, nullptr, nullptr, nullptr};
+  CgBufs B{z1, a.r, a.p, nullptr, a.t, nullptr, nullptr, nullptr, nullptr, 0, 0, 0, 0};
   const int64_t k = cg_loop<TD>(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, a.n, a.m, rns, delta, floor_,
                             a.max_iter, gs, nullptr, nullptr, prof);
   double h[2] = {0.0, 0.0};
@@ -705,6 +718,7 @@ struct ScsArgs {
   int resid_every;
   int stash_cap;   // doubles of shared memory per CTA for the SOC stash
   double* prof;    // PROF_N phase times (ns) or null
+  int64_t b_lo, b_hi, c_lo, c_hi;  // b, c are zero outside [lo, hi) (skip those loads)
 };
 
 // CG tolerance exactly as the solver graph computes it (scs.py:290-311)
@@ -758,6 +772,18 @@ struct ConeElem {
     const double s = ((v[0] + v[1]) - cs->tau * v[2]) - v[3];
     const double u2 = kind == SEG_ZERO ? s : fmax(s, 0.0);
     bw += v[4] * cs->store(base + i, s, u2);
+  }
+};
+
+// the same where b is zero on the segment (inputs: w_y, A p1, g_y, v_y)
+struct ConeElemNoB {
+  const ConeStep* cs;
+  int64_t base;
+  int kind;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[4], int64_t) {
+    const double s = ((v[0] + v[1]) - cs->tau * v[2]) - v[3];
+    const double u2 = kind == SEG_ZERO ? s : fmax(s, 0.0);
+    cs->store(base + i, s, u2);
   }
 };
 
@@ -872,7 +898,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double s[4] = {0.0, 0.0, 0.0, bwy_part};
     {
       InVec in{wy, nullptr, 0.0};
-      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev};
+      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev, a.c_lo, a.c_hi};
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = a.prof + 16;
       apply_plan<TD>(Aj, in, e, s, gs);
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = nullptr;
@@ -885,7 +911,8 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double rns = s[1];
     double cx = s[2];
     const double bwy = s[3];
-    CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c};
+    CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c, a.b_lo, a.b_hi,
+             a.c_lo, a.c_hi};
     const int64_t cgk = cg_loop<TD>(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
                                 cg_max, gs, &cx, &bax, prof);
     // tau~ = (w_tau + h.p) / (1 + h.g) with h.p = c.p1 + b.(w_y + A p1)
@@ -914,11 +941,18 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
       const DevSeg sg = K.seg[sg_i];
       if (sg.kind == SEG_SOC_LARGE) continue;
-      ConeElem f{&cs, sg.begin, sg.kind, 0.0};
-      const double* src[5] = {wy + sg.begin, W.tax + sg.begin, a.g + n + sg.begin,
-                              W.v + n + sg.begin, a.b + sg.begin};
-      bulk_stream<5>(sg.end - sg.begin, src, f);
-      bw += f.bw;
+      if (sg.end <= a.b_lo || sg.begin >= a.b_hi) {  // b == 0 here: no b.w_y term
+        ConeElemNoB f{&cs, sg.begin, sg.kind};
+        const double* src[4] = {wy + sg.begin, W.tax + sg.begin, a.g + n + sg.begin,
+                                W.v + n + sg.begin};
+        bulk_stream<4>(sg.end - sg.begin, src, f);
+      } else {
+        ConeElem f{&cs, sg.begin, sg.kind, 0.0};
+        const double* src[5] = {wy + sg.begin, W.tax + sg.begin, a.g + n + sg.begin,
+                                W.v + n + sg.begin, a.b + sg.begin};
+        bulk_stream<5>(sg.end - sg.begin, src, f);
+        bw += f.bw;
+      }
     }
     // small SOC blocks: one warp per cone, norm then projection
     {
@@ -1805,6 +1839,16 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.max_steps = max_steps;
   a.resid_every = resid_every_iter;
   a.prof = ctx->prof;
+  // zero-initialised ranges mean "no information": stream all of b / c
+  const bool bz = prob->b_nz_begin == 0 && prob->b_nz_end == 0;
+  const bool cz = prob->c_nz_begin == 0 && prob->c_nz_end == 0;
+  a.b_lo = bz ? 0 : prob->b_nz_begin;
+  a.b_hi = bz ? prob->m : prob->b_nz_end;
+  a.c_lo = cz ? 0 : prob->c_nz_begin;
+  a.c_hi = cz ? prob->n : prob->c_nz_end;
+  if (a.b_lo < 0 || a.b_hi > prob->m || a.b_lo > a.b_hi || a.c_lo < 0 || a.c_hi > prob->n ||
+      a.c_lo > a.c_hi)
+    return fail(CGB_EINVAL, "cgb_scs_run: b/c nonzero range out of bounds");
   // shared memory: conv staging of the plans, or the large-SOC stash of the
   // cone step, whichever is larger (never live together; one CTA per SM --
   // the kernel re-checks the stash need with the real grid)

@@ -248,6 +248,12 @@ def residuals(iterate: ScsIterate, problem: ConeProblem) -> tuple[float, float, 
     return float(pr), float(dr), np.inf
 
 
+def _nonzero_range(v: np.ndarray) -> tuple[int, int]:
+    """[first, last + 1) of v's nonzeros ((0, 0) when v == 0)."""
+    nz = np.flatnonzero(v)
+    return (int(nz[0]), int(nz[-1]) + 1) if len(nz) else (0, 0)
+
+
 # -- the compiled solver ("graph") ---------------------------------------------------
 
 class SolverPlan:
@@ -273,11 +279,14 @@ class SolverPlan:
         self.buf["state"] = torch.zeros(_lib.STATE_LEN, **f64)
         self.work = _lib.ScsWorkC(**{nm: t.data_ptr() for nm, t in self.buf.items()})
         ca = self.cached
+        bl, bh = _nonzero_range(problem.b)
+        cl, ch = _nonzero_range(problem.c)
         self.cprob = _lib.ScsProblemC(
             n=n, m=m, A=self.dev.handle.value, K=self.cones.handle.value,
             b=ca.b_device.data_ptr(), c=ca.c_device.data_ptr(), g=ca.g_device.data_ptr(),
             denom=ca.denom, pr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.b))),
-            dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))))
+            dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))),
+            b_nz_begin=bl, b_nz_end=bh, c_nz_begin=cl, c_nz_end=ch)
         self.csettings = settings.to_c(n)
         self.reset()
 
@@ -360,6 +369,12 @@ class SolverPlan:
                   + ar + W * 2 * n                # q = p + A^T t, p.q
                   + W * (9 * n + 5 * m))          # x, r, A^T A x, A x updates + dots
         per_check = fr + ar + W * (3 * n + 4 * m)  # A u_x, A^T u_y, c.u_x, b.u_y
+        # the loop skips b / c where they are zero (cgb_scs_problem.*_nz_*):
+        # the rhs c read and the tracked c.p / b.t dots stream only the range
+        cz = n - (self.cprob.c_nz_end - self.cprob.c_nz_begin)
+        bz = m - (self.cprob.b_nz_end - self.cprob.b_nz_begin)
+        per_iter -= W * cz
+        per_cg -= W * (cz + bz)
         return {"per_iter": per_iter, "per_cg_iter": per_cg, "per_check": per_check}
 
     def launch_bytes(self, iterations: int, cg_total: int) -> int:

@@ -26,9 +26,9 @@ def _lib_loaded():
 
 
 def test_library_is_the_native_path():
-    lib = _lib_loaded()
-    assert lib.cgb_abi_version() == 1
     from paper_1609_03488_b200 import _lib
+    lib = _lib_loaded()
+    assert lib.cgb_abi_version() == _lib.ABI_VERSION
     ctx = _lib.device_context()
     sms, per_sm, threads = ctx.geometry()
     assert sms >= 100 and per_sm >= 1 and threads >= 128
@@ -462,3 +462,30 @@ def test_kron_lowering_matches_numpy():
     M3 = 2.0 * np.kron(linop.materialize_dense(C), A)
     y3 = rng.standard_normal(M3.shape[0])
     np.testing.assert_allclose(op3.adjoint_apply(y3), M3.T @ y3, rtol=1e-12, atol=1e-11)
+
+
+def test_zero_range_skipping_is_bitwise_neutral():
+    """Skipping b / c loads over their zero ranges (cgb_scs_problem
+    b_nz_* / c_nz_*) must not change a single bit of the trajectory: the
+    same plan run with the ranges zeroed (stream everything) ends in the
+    identical state, and out-of-bounds ranges are rejected."""
+    from paper_1609_03488_b200 import _lib, canon
+    n, k = 20_000, 101
+    c, b, _ = canon.gen_deconv1d(n, k, seed=5, spikes=20)
+    prob = canon.build_deconv(canon.DeconvProblem(c, b, n=n))
+    plan = scs.build_scs_graph(prob, scs.ScsSettings(eps=1e-3, max_iters=5000))
+    cp = plan.cprob
+    assert (cp.b_nz_begin, cp.c_nz_begin, cp.c_nz_end) == (n + 1, n, n + 1)
+    plan.reset()
+    plan.run(300)
+    skipped = plan.state().copy()
+    saved = (cp.b_nz_begin, cp.b_nz_end, cp.c_nz_begin, cp.c_nz_end)
+    cp.b_nz_begin = cp.b_nz_end = cp.c_nz_begin = cp.c_nz_end = 0
+    plan.reset()
+    plan.run(300)
+    full = plan.state().copy()
+    assert np.array_equal(skipped, full)
+    cp.b_nz_begin, cp.b_nz_end = 5, prob.A.rows + 1
+    with pytest.raises(_lib.CgbError):
+        plan.run(1)
+    cp.b_nz_begin, cp.b_nz_end, cp.c_nz_begin, cp.c_nz_end = saved
