@@ -137,3 +137,31 @@ def test_logreg_stuffing_permutation_is_a_bijection():
     perm = prob.A.expr.child.children[1].left.matrix   # Scale(-1, VStack([.., P @ B]))
     assert perm.nnz == 42 and (np.sort(perm.indices) == np.arange(42)).all()
     assert (perm.sum(axis=0) == 1).all() and (perm.sum(axis=1) == 1).all()
+
+
+def test_nonzero_ranges_of_stuffed_vectors():
+    """The b / c nonzero ranges the loop uses to skip loads
+    (cgb_scs_problem.b_nz_* / c_nz_*): exact first/last nonzero, (0, 0) for
+    an all-zero vector (= "no information" at the ABI: stream everything)."""
+    from paper_1609_03488_b200 import canon, scs
+    assert scs._nonzero_range(np.zeros(5)) == (0, 0)
+    assert scs._nonzero_range(np.array([0.0, 0.0, 3.0, 0.0, -1.0, 0.0])) == (2, 5)
+    assert scs._nonzero_range(np.array([1.0])) == (0, 1)
+    n, k = 50, 7
+    rng = np.random.default_rng(0)
+    sig = rng.standard_normal(n + k - 1)
+    c = np.abs(rng.standard_normal(k)) + 0.1
+    prob = canon.build_deconv(canon.DeconvProblem(c, sig, n=n))
+    # stuffed deconv: b = (0_n, 0, -sig), c = (0_n, 1)
+    assert scs._nonzero_range(prob.b) == (n + 1, 2 * n + k)
+    assert scs._nonzero_range(prob.c) == (n, n + 1)
+
+
+def test_abi_problem_struct_carries_ranges():
+    from paper_1609_03488_b200 import _lib
+    names = [f[0] for f in _lib.ScsProblemC._fields_]
+    assert names[-4:] == ["b_nz_begin", "b_nz_end", "c_nz_begin", "c_nz_end"]
+    assert ctypes.sizeof(_lib.ScsProblemC) == 8 * 2 + 8 * 5 + 8 * 3 + 8 * 4
+    hdr = open(os.path.join(ROOT, "include", "cgb200.h")).read()
+    for nm in names[-4:]:
+        assert nm in hdr
