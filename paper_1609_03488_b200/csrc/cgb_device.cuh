@@ -31,7 +31,9 @@
 #define CGB_DENSE_UNROLL 4   // dense GEMV: column chunks unrolled per row group
 #endif
 #define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
+#ifndef CGB_U
 #define CGB_U 8              // elements per thread per batch in streaming loops
+#endif
 
 namespace cgb {
 
