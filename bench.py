@@ -1,36 +1,41 @@
 #!/usr/bin/env python
 """Benchmark of the B200 conegraph solver path (driver contract).
 
-Default workload (BASELINE.json configs[1]): 1-D nonnegative deconvolution,
-signal n = 1e6, Gaussian kernel length 101, stuffed exactly like the
-reference's build_deconv (variables n+1, constraints 2n+k), solved to
-eps = 1e-3.  ``--workload`` selects the other BASELINE configs (their lines
-are evidence for DESIGN.md; the driver runs the default):
+Default workload (BASELINE.json configs[2], the config the north star's
+>= 50x time-to-eps target is quoted on): 2-D nonnegative image
+deconvolution, 4096 x 4096 image, 15 x 15 Gaussian blur, stuffed like the
+reference's build_deconv (variables N+1, constraints N+1+(4110^2)), eps =
+1e-3.  ``--workload`` selects the other BASELINE configs:
+  deconv2d      configs[2]  (default)
   lasso_dense   configs[0]  dense lasso A 1000 x 500, lam = 0.1
-  deconv1d      configs[1]  (default)
-  deconv2d      configs[2]  2-d nonneg deconvolution 4096 x 4096, 15 x 15 blur
-  lasso_sparse  configs[3]  sparse lasso A 8e6 x 1e6 CSR, density 1e-5 (1 GPU)
+  deconv1d      configs[1]  1-d nonneg deconvolution, n = 1e6, kernel 101
+  lasso_sparse  configs[3]  sparse lasso A 8e6 x 1e6 CSR, density 1e-5;
+                            with --gpus N the rows of A are sharded over N ranks
   logreg        configs[4]  l1 logistic regression, 2 exp cones per sample, A 2e5 x 2e3
   soc_ls        configs[4]  SOC-constrained least squares, dense A 2e5 x 2e3
 
-A *step* is one complete solve to eps from a cold start: the one-time
-setup solve g = (I+Q_z)^{-1} h followed by the splitting iterations until
-the device-latched status says solved.  ``value`` is ADMM (splitting)
-iterations per second over the K timed steps with the problem data
-resident in HBM (all ranks summed); ``time_to_eps_s`` is the mean step
-time.  ``e2e`` is the same metric through the public API (``scs.solve`` on
-numpy inputs: host->device copies, operator / cone compilation, setup,
-solve, device->host copy of x, y, s) per step.
+A *step* is one cold start of the solver with the problem data resident in
+HBM: the one-time setup solve g = (I+Q_z)^{-1} h, then the splitting
+iterations from u = v = (0, 0, 1) -- either to eps (small workloads) or a
+bounded block of ``step_iters`` iterations (deconv2d: 2000 of the ~9e4 to
+eps, so K steps fit the driver's step limit).  ``value`` is ADMM
+(splitting) iterations per second over the K timed steps (all ranks
+summed, time = max over ranks).  ``time_to_eps_s`` is measured once, by one
+full cold solve to eps after the timed steps.  ``e2e`` is the same metric
+through the public API (``scs.solve`` on numpy inputs: host->device copies,
+operator / cone compilation, setup, the same bounded iterations, and the
+device->host copy of x, y, s) per step.
 
 ``--impl reference`` times the reference algorithm's CPU implementation
 (the numpy restatement in oracle/, pinned to the real reference's golden
-vectors) on the host cores: rank 0 only, a bounded sample of splitting
-iterations of the same instance per step, same metric and unit.
+vectors; the problem is stuffed by oracle/canon_ref.py, nothing of the
+product is imported) on the host cores: rank 0 only, after the oracle's
+own setup solve (untimed), each step a bounded block of splitting
+iterations of the same instance, same metric and unit.
 
-Multi-GPU: these workloads are single structured operators, which the
-north star keeps on one GPU, so N > 1 runs N independent replicas (one
-solve per rank, no data-path collective; "scaling": "weak"); time is the
-max over ranks of the per-rank device time.
+Multi-GPU: lasso_sparse is row-sharded over the ranks;
+the single-operator workloads are kept on one GPU by the north star, so
+N > 1 runs N independent replicas of them (no data-path collective).
 """
 
 from __future__ import annotations
@@ -44,44 +49,83 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+EPS = 1e-3
+MAX_ITERS = 200_000
+SEED = 0
+NOISE_SIGMA = 0.01
+METRIC = "ADMM iterations/s (time-to-eps=1e-3 in time_to_eps_s)"
 N_SIGNAL = 1_000_000
 K_KERNEL = 101
-EPS = 1e-3
-MAX_ITERS = 100_000
-SEED = 0
-METRIC = "ADMM iterations/s (time-to-eps=1e-3 in time_to_eps_s)"
+
+
+# ---------------------------------------------------------------------------
+# data generators (numpy only; the same arithmetic as canon.gaussian_kernel,
+# canon.gaussian_kernel2d and canon.gen_logreg -- tests/test_host.py checks
+# they agree -- so the reference arm needs nothing from the product)
+# ---------------------------------------------------------------------------
+
+def gaussian_kernel(n: int) -> np.ndarray:
+    """Centered Gaussian kernel of length n, std n/10, unit sum (canon.py:135-139)."""
+    i = np.arange(n, dtype=np.float64)
+    k = np.exp(-((i - n / 2.0) ** 2) / (2.0 * (n / 10.0) ** 2))
+    return k / k.sum()
+
+
+def gaussian_kernel2d(kh: int, kw: int) -> np.ndarray:
+    """Separable centered Gaussian blur (std k/6 per axis), unit sum."""
+    def axis(k):
+        i = np.arange(k, dtype=np.float64)
+        return np.exp(-((i - (k - 1) / 2.0) ** 2) / (2.0 * (k / 6.0) ** 2))
+    K = np.outer(axis(kh), axis(kw))
+    return K / K.sum()
+
+
+def gen_logreg(m: int, n: int, seed: int, density: float = 0.1):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((m, n)) / np.sqrt(n)
+    w = rng.standard_normal(n) * (rng.uniform(size=n) < density) * 3.0
+    pr = 1.0 / (1.0 + np.exp(-(A @ w)))
+    y = np.where(rng.uniform(size=m) < pr, 1.0, -1.0)
+    return A, y, w
+
+
+def _instance(n: int):
+    """deconv1d instance: Gaussian kernel 101, 50 nonnegative spikes, noise 0.01."""
+    rng = np.random.default_rng(SEED)
+    c = gaussian_kernel(K_KERNEL)
+    x_hat = np.zeros(n)
+    pos = rng.choice(n, size=min(50, n), replace=False)
+    x_hat[pos] = rng.uniform(0.0, 10.0, size=len(pos))
+    b = np.convolve(c, x_hat) + NOISE_SIGMA * rng.standard_normal(n + K_KERNEL - 1)
+    return c, b, x_hat
 
 
 # ---------------------------------------------------------------------------
 # workloads (host-generated, bit-identical for both arms)
 # ---------------------------------------------------------------------------
 
-def _instance(n: int):
-    """deconv1d instance (canon.gen_deconv1d's recipe: Gaussian kernel, 50
-    nonnegative spikes, noise 0.01), generated on the host."""
-    import numpy as np
-    from paper_1609_03488_b200 import canon
-    rng = np.random.default_rng(SEED)
-    c = canon.gaussian_kernel(K_KERNEL)
-    x_hat = np.zeros(n)
-    pos = rng.choice(n, size=min(50, n), replace=False)
-    x_hat[pos] = rng.uniform(0.0, 10.0, size=len(pos))
-    b = np.convolve(c, x_hat) + canon.NOISE_SIGMA * rng.standard_normal(n + K_KERNEL - 1)
-    return c, b, x_hat
-
-
 class Workload:
     name = ""
+    baseline_config = -1
     eps = EPS
+    step_iters = 0   # 0: a step runs to eps; else a bounded block of iterations
+    cpu_iters = 2    # splitting iterations of the bench's cpu_baseline sample
+    ref_iters = 1    # splitting iterations per --impl reference step
 
     def config(self) -> dict:
         raise NotImplementedError
 
     def problem(self):
-        """The stuffed cone problem through the public API, from host data."""
+        """The stuffed cone problem through the product's public API."""
+        raise NotImplementedError
+
+    def oracle_problem(self):
+        """The same stuffed problem built by oracle/canon_ref.py."""
         raise NotImplementedError
 
     def h2d_bytes(self) -> int:
@@ -90,8 +134,11 @@ class Workload:
 
 class Deconv1D(Workload):
     name = "deconv1d_nonneg"
+    baseline_config = 1
+    cpu_iters = 20
+    ref_iters = 10
 
-    def __init__(self, n: int):
+    def __init__(self, n: int = N_SIGNAL):
         self.n = n
         self._d = None
 
@@ -110,6 +157,11 @@ class Deconv1D(Workload):
         c, b, _ = self.data()
         return canon.build_deconv(canon.DeconvProblem(c, b, n=self.n))
 
+    def oracle_problem(self):
+        from oracle import canon_ref
+        c, b, _ = self.data()
+        return canon_ref.build_deconv(c, b, self.n)
+
     def h2d_bytes(self):
         n = self.n
         return 8 * (K_KERNEL + (n + K_KERNEL - 1)) + 8 * ((2 * n + K_KERNEL) + (n + 1))
@@ -117,6 +169,10 @@ class Deconv1D(Workload):
 
 class Deconv2D(Workload):
     name = "deconv2d_nonneg"
+    baseline_config = 2
+    step_iters = 2000
+    cpu_iters = 2
+    ref_iters = 1
 
     def __init__(self, h: int = 4096, w: int = 4096, k: int = 15):
         self.h, self.w, self.k = h, w, k
@@ -124,16 +180,14 @@ class Deconv2D(Workload):
 
     def data(self):
         if self._d is None:
-            import numpy as np
             import scipy.signal
-            from paper_1609_03488_b200 import canon
             rng = np.random.default_rng(SEED)
-            K = canon.gaussian_kernel2d(self.k, self.k)
+            K = gaussian_kernel2d(self.k, self.k)
             x = np.zeros(self.h * self.w)
             pos = rng.choice(self.h * self.w, size=200, replace=False)
             x[pos] = rng.uniform(0.0, 10.0, size=200)
             full = scipy.signal.fftconvolve(x.reshape(self.h, self.w), K, mode="full")
-            b = full.reshape(-1) + canon.NOISE_SIGMA * rng.standard_normal(full.size)
+            b = full.reshape(-1) + NOISE_SIGMA * rng.standard_normal(full.size)
             self._d = (K, b, x)
         return self._d
 
@@ -149,6 +203,11 @@ class Deconv2D(Workload):
         K, b, _ = self.data()
         return canon.build_deconv2d(canon.Deconv2DProblem(K, b, (self.h, self.w)))
 
+    def oracle_problem(self):
+        from oracle import canon_ref
+        K, b, _ = self.data()
+        return canon_ref.build_deconv2d(K, b, (self.h, self.w))
+
     def h2d_bytes(self):
         N = self.h * self.w
         M = (self.h + self.k - 1) * (self.w + self.k - 1)
@@ -157,6 +216,9 @@ class Deconv2D(Workload):
 
 class LassoDense(Workload):
     name = "lasso_dense"
+    baseline_config = 0
+    cpu_iters = 200
+    ref_iters = 50
 
     def __init__(self, m: int = 1000, n: int = 500, lam: float = 0.1):
         self.m, self.n, self.lam = m, n, lam
@@ -164,7 +226,6 @@ class LassoDense(Workload):
 
     def data(self):
         if self._d is None:
-            import numpy as np
             rng = np.random.default_rng(SEED)
             A = rng.standard_normal((self.m, self.n))
             x = rng.standard_normal(self.n) * (rng.uniform(size=self.n) < 0.1)
@@ -182,12 +243,21 @@ class LassoDense(Workload):
         A, b = self.data()
         return canon.build_lasso(canon.LassoProblem(linop.dense(A), b, self.lam))
 
+    def oracle_problem(self):
+        from oracle import canon_ref
+        from oracle.exprs_ref import DenseMatrix
+        A, b = self.data()
+        return canon_ref.build_lasso(DenseMatrix(A), b, self.lam)
+
     def h2d_bytes(self):
         return 8 * (self.m * self.n * 2 + self.m + 2 * self.n + self.m + 2)
 
 
 class LassoSparse(Workload):
     name = "lasso_sparse"
+    baseline_config = 3
+    cpu_iters = 3
+    ref_iters = 1
 
     def __init__(self, m: int = 8_000_000, n: int = 1_000_000, density: float = 1e-5):
         self.m, self.n, self.density = m, n, density
@@ -195,7 +265,6 @@ class LassoSparse(Workload):
 
     def data(self):
         if self._d is None:
-            import numpy as np
             import scipy.sparse
             rng = np.random.default_rng(SEED)
             nnz = int(self.m * self.n * self.density)
@@ -223,12 +292,18 @@ class LassoSparse(Workload):
         return {"workload": self.name, "baseline_config": 3, "A": [self.m, self.n],
                 "nnz": int(A.nnz), "lam": lam, "eps": self.eps,
                 "stuffed_n": 2 * self.n + 1, "stuffed_m": 2 * self.n + self.m + 2,
-                "seed": SEED, "sharding": "1 GPU (row-sharded multi-GPU path: DESIGN.md §8e)"}
+                "seed": SEED}
 
     def problem(self):
         from paper_1609_03488_b200 import canon, linop
         A, b, lam = self.data()
         return canon.build_lasso(canon.LassoProblem(linop.sparse_csc(A), b, lam))
+
+    def oracle_problem(self):
+        from oracle import canon_ref
+        from oracle.exprs_ref import SparseMatrix
+        A, b, lam = self.data()
+        return canon_ref.build_lasso(SparseMatrix(A), b, lam)
 
     def h2d_bytes(self):
         A, _, _ = self.data()
@@ -237,6 +312,9 @@ class LassoSparse(Workload):
 
 class LogReg(Workload):
     name = "logreg_exp"
+    baseline_config = 4
+    cpu_iters = 2
+    ref_iters = 1
 
     def __init__(self, m: int = 200_000, n: int = 2_000, lam: float = 0.01):
         self.m, self.n, self.lam = m, n, lam
@@ -244,14 +322,15 @@ class LogReg(Workload):
 
     def data(self):
         if self._d is None:
-            from paper_1609_03488_b200 import canon
-            A, y, _ = canon.gen_logreg(self.m, self.n, seed=SEED)
+            A, y, _ = gen_logreg(self.m, self.n, seed=SEED)
             self._d = (A, y)
         return self._d
 
+    def dims(self):
+        return 2 * self.n + 3 * self.m, 2 * self.n + self.m + 6 * self.m
+
     def config(self):
-        from paper_1609_03488_b200 import canon
-        ns, ms = canon.logreg_dims(self.m, self.n)
+        ns, ms = self.dims()
         return {"workload": self.name, "baseline_config": 4, "A": [self.m, self.n],
                 "lam": self.lam, "exp_cones": 2 * self.m, "eps": self.eps, "stuffed_n": ns,
                 "stuffed_m": ms, "seed": SEED}
@@ -261,14 +340,21 @@ class LogReg(Workload):
         A, y = self.data()
         return canon.build_logreg(canon.LogRegProblem(A, y, self.lam))
 
+    def oracle_problem(self):
+        from oracle import canon_ref
+        A, y = self.data()
+        return canon_ref.build_logreg(A, y, self.lam)
+
     def h2d_bytes(self):
-        from paper_1609_03488_b200 import canon
-        ns, ms = canon.logreg_dims(self.m, self.n)
+        ns, ms = self.dims()
         return 8 * (2 * self.m * self.n) + 12 * 6 * self.m + 8 * (ns + ms)
 
 
 class SocLs(Workload):
     name = "soc_ls"
+    baseline_config = 4
+    cpu_iters = 3
+    ref_iters = 2
 
     def __init__(self, m: int = 200_000, n: int = 2_000, radius: float = 1.0):
         self.m, self.n, self.radius = m, n, radius
@@ -276,7 +362,6 @@ class SocLs(Workload):
 
     def data(self):
         if self._d is None:
-            import numpy as np
             rng = np.random.default_rng(SEED)
             A = rng.standard_normal((self.m, self.n)) / np.sqrt(self.m)
             b = A @ rng.standard_normal(self.n) + 0.1 * rng.standard_normal(self.m) / np.sqrt(self.m)
@@ -293,23 +378,25 @@ class SocLs(Workload):
         A, b = self.data()
         return canon.build_soc_ls(canon.SocLsProblem(linop.dense(A), b, self.radius))
 
+    def oracle_problem(self):
+        from oracle import canon_ref
+        from oracle.exprs_ref import DenseMatrix
+        A, b = self.data()
+        return canon_ref.build_soc_ls(DenseMatrix(A), b, self.radius)
+
     def h2d_bytes(self):
         return 8 * (2 * self.m * self.n + 2 * (self.m + self.n + 2) + self.n + 1)
+
+
+WORKLOADS = {"deconv2d": Deconv2D, "deconv1d": Deconv1D, "lasso_dense": LassoDense,
+             "lasso_sparse": LassoSparse, "logreg": LogReg, "soc_ls": SocLs}
 
 
 def make_workload(args) -> Workload:
     if args.workload == "deconv1d":
         return Deconv1D(args.n)
-    if args.workload == "deconv2d":
-        return Deconv2D()
-    if args.workload == "lasso_dense":
-        return LassoDense()
-    if args.workload == "lasso_sparse":
-        return LassoSparse()
-    if args.workload == "logreg":
-        return LogReg()
-    if args.workload == "soc_ls":
-        return SocLs()
+    if args.workload in WORKLOADS:
+        return WORKLOADS[args.workload]()
     raise SystemExit(f"unknown workload {args.workload}")
 
 
@@ -319,22 +406,37 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="deconv1d",
-                    choices=["deconv1d", "deconv2d", "lasso_dense", "lasso_sparse", "logreg",
-                             "soc_ls"])
+    ap.add_argument("--workload", default="deconv2d", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=N_SIGNAL, help="deconv1d signal length")
+    ap.add_argument("--step-iters", type=int, default=-1,
+                    help="splitting iterations per step (0 = to eps; default per workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-solve", action="store_true",
+                    help="skip the one full solve that measures time_to_eps_s")
     ap.add_argument("--cpu-iters", type=int, default=0,
                     help="splitting iterations per CPU sample (0 = workload default)")
     return ap.parse_args()
 
 
-def _config(wl: Workload, n_gpus: int) -> dict:
+def _step_iters(args, wl: Workload) -> int:
+    return wl.step_iters if args.step_iters < 0 else args.step_iters
+
+
+def _config(wl: Workload, n_gpus: int, step_iters: int, parallelism: str | None = None) -> dict:
     cfg = wl.config()
-    cfg.update({"step": "one full solve to eps (setup solve + splitting iterations, cold start)",
-                "l2": "flushed between timed steps (256 MiB write)",
-                "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single"})
+    if step_iters > 0:
+        step = (f"one cold start: setup solve + {step_iters} splitting iterations "
+                f"(bounded; time to eps from one full solve, time_to_eps_s)")
+    else:
+        step = "one full solve to eps (setup solve + splitting iterations, cold start)"
+    cfg.update({"step": step, "step_iters": step_iters,
+                "l2": "flushed between timed steps (256 MiB write); every iterate vector "
+                      "exceeds L2 as well" if step_iters else
+                      "flushed between timed steps (256 MiB write)",
+                "parallelism": parallelism or (f"replicas{n_gpus} (independent solves, no "
+                                               f"data-path collective)" if n_gpus > 1
+                                               else "single")})
     return cfg
 
 
@@ -406,68 +508,70 @@ def _dist():
     return world, rank, local
 
 
+def _peaks() -> dict:
+    """HBM peak from the driver's MEASURED_PEAKS.json and the measured FP64
+    DFMA peak (profiles/fp64_peak.json, tools/fp64_peak.cu), with fallbacks."""
+    out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)",
+           "fp64_tflops": 37.0, "fp64_src": "fallback (nominal B200 FP64 vector)"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            out["hbm_gbs"] = float(json.load(open(p))["hbm_gbs"])
+            out["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+        except Exception:  # noqa: BLE001
+            pass
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        try:
+            out["fp64_tflops"] = float(json.load(open(p))["dfma_tflops"])
+            out["fp64_src"] = "measured (profiles/fp64_peak.json)"
+        except Exception:  # noqa: BLE001
+            pass
+    return out
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the CPU implementation of the path (oracle port)
 # ---------------------------------------------------------------------------
 
-class _Tree:
-    """The stuffed problem as a duck-typed tree the oracle walks."""
-
-    def __init__(self, prob):
-        self.A, self.b, self.c, self.K = prob.A.expr, prob.b, prob.c, prob.K
-
-
-def _cpu_cores_used() -> int:
-    """Host threads the oracle can use: numpy's FFTs are single-threaded, its
-    dot products / norms run in OpenBLAS with this many threads."""
-    try:
-        from threadpoolctl import threadpool_info
-        blas = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
-        if blas:
-            return int(max(blas))
-    except Exception:  # noqa: BLE001 - reporting only
-        pass
+def _cpu_threads() -> int:
     return os.cpu_count() or 1
 
 
-def _default_cpu_iters(wl: Workload) -> int:
-    return {"deconv1d_nonneg": 20, "deconv2d_nonneg": 2, "lasso_dense": 200,
-            "lasso_sparse": 3, "logreg_exp": 2, "soc_ls": 3}.get(wl.name, 10)
+class _OracleRun:
+    """The oracle's own setup solve and splitting loop on one workload
+    (problem stuffed by oracle/canon_ref.py: no product code involved)."""
 
-
-def _oracle_cached(wl: Workload, own_setup: bool):
-    """The oracle's setup (its own solve when affordable, else the device's
-    cached g -- the per-iteration work does not depend on it)."""
-    import numpy as np
-    from oracle import scs_ref
-    p = _Tree(wl.problem())
-    s = scs_ref.ScsOracleSettings(eps=wl.eps, max_iters=MAX_ITERS)
-    if own_setup:
+    def __init__(self, wl: Workload):
+        import scipy.fft
+        from oracle import scs_ref
+        self.scs_ref = scs_ref
+        self.workers = scipy.fft.set_workers(_cpu_threads())
+        self.workers.__enter__()   # scipy FFTs (2-d convolutions) on every host core
+        self.p = wl.oracle_problem()
+        self.s = scs_ref.ScsOracleSettings(eps=wl.eps, max_iters=MAX_ITERS)
         t0 = time.perf_counter()
-        cached = scs_ref.prepare_subspace(p, s.setup_cg_tol, s.cg_max_iter)
-        return p, s, cached, time.perf_counter() - t0
-    from paper_1609_03488_b200 import scs
-    pc = scs.prepare_subspace(wl.problem(), s.setup_cg_tol, s.cg_max_iter)
-    cached = scs_ref.Cached(np.asarray(pc.h), np.asarray(pc.g), float(pc.denom),
-                            s.setup_cg_tol, s.cg_max_iter, int(pc.setup_cg_iters))
-    return p, s, cached, None
+        self.cached = scs_ref.prepare_subspace(self.p, self.s.setup_cg_tol, self.s.cg_max_iter)
+        self.setup_s = time.perf_counter() - t0
+        self.it = scs_ref.iterate(self.p, self.s, self.cached, MAX_ITERS)
+
+    def run(self, iters: int) -> float:
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            next(self.it)
+        return time.perf_counter() - t0
 
 
-def cpu_sample(wl: Workload, iters: int, warmup_iters: int = 1):
-    """Time the oracle's splitting iterations on the host (setup excluded
-    from the rate; reported separately when the oracle ran it)."""
-    from oracle import scs_ref
-    own = wl.name in ("deconv1d_nonneg", "lasso_dense")
-    p, s, cached, setup_s = _oracle_cached(wl, own)
-    it = scs_ref.iterate(p, s, cached, warmup_iters + iters)
-    for _ in range(warmup_iters):
-        next(it)
-    t0 = time.perf_counter()
-    done = 0
-    for _k, _st in it:
-        done += 1
-    dt = time.perf_counter() - t0
-    return {"setup_s": setup_s, "iters": done, "seconds": dt, "iters_per_s": done / dt}
+def _oracle_full_solve_record(wl: Workload) -> dict | None:
+    """The oracle's own full solve of this exact instance, when one was run
+    (profiles/oracle_full_solves.json)."""
+    p = os.path.join(ROOT, "profiles", "oracle_full_solves.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get(wl.name)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def run_reference(args) -> None:
@@ -475,35 +579,28 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     wl = make_workload(args)
-    iters = args.cpu_iters or max(1, _default_cpu_iters(wl) // 2)
-    from oracle import scs_ref
-    own = wl.name in ("deconv1d_nonneg", "lasso_dense")
-    p, s, cached, setup_s = _oracle_cached(wl, own)
-    state_it = scs_ref.iterate(p, s, cached, MAX_ITERS)
-    times = []
-    for step in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        for _ in range(iters):
-            next(state_it)
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            times.append(dt)
+    iters = args.cpu_iters or wl.ref_iters
+    orc = _OracleRun(wl)
+    for _ in range(min(args.warmup, 1)):   # the CPU has no warm-up beyond the first
+        orc.run(iters)
+    times = [orc.run(iters) for _ in range(args.steps)]
     total = sum(times)
     value = iters * len(times) / total
-    setup_note = (f"after the oracle's own setup solve ({setup_s:.1f} s, untimed)"
-                  if setup_s is not None else "from the device's cached setup solution")
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config(wl, 1),
-        "setup_s": setup_s,
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": _cpu_cores_used(),
+        "data": "synthetic", "config": _config(wl, 1, _step_iters(args, wl)),
+        "setup_s": orc.setup_s,
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": _cpu_threads(),
                          "kind": "port",
-                         "sample": f"{iters} splitting iterations per step of the "
-                                   f"{wl.name} instance {setup_note}; numpy restatement of "
-                                   f"conegraph scs.py (FFT convolution as linop.py)"},
+                         "sample": f"{iters} splitting iteration(s) per step of the {wl.name} "
+                                   f"instance after the oracle's own setup solve "
+                                   f"({orc.setup_s:.1f} s, untimed); numpy restatement of "
+                                   f"conegraph scs.py (oracle/scs_ref.py), problem stuffed by "
+                                   f"oracle/canon_ref.py; BLAS and scipy FFTs on "
+                                   f"{_cpu_threads()} host threads"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -524,12 +621,16 @@ def run_b200(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload == "lasso_sparse" and world > 1:
+        return run_b200_sharded(args)
     from paper_1609_03488_b200 import _lib, scs
 
     wl = make_workload(args)
+    S = _step_iters(args, wl)
+    cap = S if S > 0 else MAX_ITERS
     settings = scs.ScsSettings(eps=wl.eps, max_iters=MAX_ITERS)
 
-    # resident-data arm: compile once (graph build), then time setup + solve
+    # resident-data arm: compile once (graph build), then time setup + loop
     prob = wl.problem()
     t0 = time.perf_counter()
     plan = scs.build_scs_graph(prob, settings)
@@ -538,13 +639,13 @@ def run_b200(args) -> None:
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    def one_step():
+    def one_step(max_steps: int):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
         plan.resetup()
         plan.reset()
         ev[1].record(stream)
-        plan.run(settings.max_iters)
+        plan.run(max_steps)
         ev[2].record(stream)
         torch.cuda.synchronize()
         st = plan.state()
@@ -553,7 +654,7 @@ def run_b200(args) -> None:
 
     for _ in range(args.warmup):
         flush.zero_()
-        one_step()
+        one_step(cap)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -562,7 +663,7 @@ def run_b200(args) -> None:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            results.append(one_step())
+            results.append(one_step(cap))
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -574,15 +675,27 @@ def run_b200(args) -> None:
     total_s, total_iters = aggregate(sum(step_s), sum(iters), "cuda")
     value = total_iters / total_s
 
-    # roofline of the dominant kernel (k_scs: the splitting loop)
-    launch_bytes = [plan.launch_bytes(i, c_) for i, c_ in zip(iters, cgs)]
-    achieved = sum(launch_bytes) / sum(kern_s) / 1e9
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(peaks_path):
-        peak = float(json.load(open(peaks_path))["hbm_gbs"])
-        peak_src = "measured"
+    # time to eps: one full cold solve (outside the timed steps when bounded)
+    if S > 0 and not args.no_full_solve:
+        flush.zero_()
+        torch.cuda.synchronize()
+        full = one_step(MAX_ITERS)
     else:
-        peak, peak_src = 6650.0, "fallback"
+        full = results[0] if S == 0 else None
+    tte = None
+    if full is not None:
+        tte = {"time_to_eps_s": full[0] if S > 0 else statistics.mean(step_s),
+               "iterations_to_eps": full[2], "cg_iterations": full[3],
+               "status": {1.0: "solved", 2.0: "infeasible", 3.0: "unbounded"}.get(
+                   full[4], "not converged"),
+               "loop_s": full[1]}
+
+    # roofline of the dominant kernel (k_scs: the splitting loop)
+    peaks = _peaks()
+    launch_bytes = [plan.launch_bytes(i, c_) for i, c_ in zip(iters, cgs)]
+    launch_flops = [plan.launch_flops(i, c_) for i, c_ in zip(iters, cgs)]
+    achieved = sum(launch_bytes) / sum(kern_s) / 1e9
+    fp64_tflops = sum(launch_flops) / sum(kern_s) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"k_scs_traffic_{args.workload}.json")
     if os.path.exists(tp):
@@ -598,6 +711,7 @@ def run_b200(args) -> None:
     # end-to-end arm: public API on host (numpy) buffers, per step
     e2e = None
     if not args.no_e2e:
+        e2e_settings = scs.ScsSettings(eps=wl.eps, max_iters=cap)
         e2e_times = []
         d2h = 0
         e2e_status = None
@@ -608,7 +722,7 @@ def run_b200(args) -> None:
             if world > 1:
                 torch.distributed.barrier()
             t0 = time.perf_counter()
-            sol = scs.solve(wl.problem(), settings)
+            sol = scs.solve(wl.problem(), e2e_settings)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             d2h = 8 * (len(sol.x) + len(sol.y) + len(sol.s))
@@ -619,27 +733,37 @@ def run_b200(args) -> None:
         e2e_s, e2e_it = aggregate(sum(t for t, _ in e2e_times),
                                   sum(i for _, i in e2e_times), "cuda")
         e2e = {"value": e2e_it / e2e_s, "unit": "iter/s", "h2d_bytes_per_step": wl.h2d_bytes(),
-               "d2h_bytes_per_step": d2h, "time_to_eps_s": e2e_s / len(e2e_times),
-               "status": e2e_status, "pobj": pobj}
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s / len(e2e_times),
+               "iterations_per_step": e2e_times[0][1], "status": e2e_status,
+               "pobj": pobj}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        iters_cpu = args.cpu_iters or _default_cpu_iters(wl)
-        cs = cpu_sample(wl, iters_cpu)
-        per_it = cs["seconds"] / cs["iters"]
-        setup_note = (f"after the oracle's own setup solve ({cs['setup_s']:.1f} s)"
-                      if cs["setup_s"] is not None else
-                      "from the device's cached setup solution (the oracle's own setup "
-                      "solve is outside the bounded sample)")
-        cpu = {"value": cs["iters_per_s"], "unit": "iter/s", "cores": _cpu_cores_used(),
+        iters_cpu = args.cpu_iters or wl.cpu_iters
+        orc = _OracleRun(wl)
+        orc.run(1)
+        dt = orc.run(iters_cpu)
+        per_it = dt / iters_cpu
+        rec = _oracle_full_solve_record(wl)
+        cpu = {"value": iters_cpu / dt, "unit": "iter/s", "cores": _cpu_threads(),
                "kind": "port",
-               "sample": f"{cs['iters']} splitting iterations of the same {wl.name} instance "
-                         f"{setup_note}; numpy restatement of conegraph scs.py (FFT "
-                         f"convolutions single-threaded, dot products in OpenBLAS threads; "
-                         f"host has {os.cpu_count()} cpus)",
-               "setup_s": cs["setup_s"],
-               "time_to_eps_s_extrapolated": (cs["setup_s"] or 0.0)
-               + per_it * statistics.mean(iters)}
+               "sample": f"{iters_cpu} splitting iterations (after 1 untimed) of the same "
+                         f"{wl.name} instance after the oracle's own setup solve "
+                         f"({orc.setup_s:.1f} s); numpy restatement of conegraph scs.py "
+                         f"(oracle/scs_ref.py), problem stuffed by oracle/canon_ref.py; BLAS "
+                         f"and scipy FFTs on {_cpu_threads()} host threads",
+               "setup_s": orc.setup_s}
+        if rec is not None:
+            cpu["time_to_eps_s_measured"] = rec.get("seconds")
+            cpu["iterations_to_eps_oracle"] = rec.get("iterations")
+            cpu["measured_where"] = rec.get("where")
+        if tte is not None:
+            basis = rec.get("iterations") if rec else tte["iterations_to_eps"]
+            cpu["time_to_eps_s_extrapolated"] = orc.setup_s + per_it * basis
+            cpu["extrapolation_basis"] = ("the oracle's own iteration count to eps "
+                                          "(profiles/oracle_full_solves.json)" if rec else
+                                          "the device's iteration count (the oracle's own "
+                                          "full solve is infeasible at this size)")
 
     if rank != 0:
         if world > 1:
@@ -649,16 +773,23 @@ def run_b200(args) -> None:
         "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(step_s),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config(wl, world),
-        "time_to_eps_s": statistics.mean(step_s),
-        "iterations_to_eps": iters[0], "avg_cg_iterations": cgs[0] / max(1, iters[0]),
+        "data": "synthetic", "config": _config(wl, world, S),
+        "time_to_eps_s": tte["time_to_eps_s"] if tte else None,
+        "iterations_to_eps": tte["iterations_to_eps"] if tte else None,
+        "full_solve": tte,
+        "iterations_per_step": iters[0], "avg_cg_iterations": cgs[0] / max(1, iters[0]),
         "status": sorted(statuses), "graph_build_s": build_s,
         "e2e": e2e,
-        "roofline": {"bound": "hbm", "kernel": "k_scs", "achieved": achieved, "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+        "roofline": {"bound": "hbm", "kernel": "k_scs", "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "peak_source": peaks["hbm_src"],
+                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                      "traffic": traffic,
                      "algorithmic_bytes_per_launch": statistics.mean(launch_bytes),
-                     "launch_ms": 1e3 * statistics.mean(kern_s)},
+                     "launch_ms": 1e3 * statistics.mean(kern_s),
+                     "fp64": {"achieved": fp64_tflops, "peak": peaks["fp64_tflops"],
+                              "peak_source": peaks["fp64_src"], "unit": "TFLOP/s",
+                              "frac": fp64_tflops / peaks["fp64_tflops"],
+                              "algorithmic_flops_per_launch": statistics.mean(launch_flops)}},
         "cpu_baseline": cpu,
         "gpu_launches": 2 * args.steps,  # k_inner (setup) + k_scs (loop) per step
         "clocks": clk.summary(),
@@ -666,6 +797,12 @@ def run_b200(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_b200_sharded(args) -> None:
+    """configs[3] row-sharded over the ranks (see shard.py)."""
+    from paper_1609_03488_b200 import shard  # noqa: F401  (built in DESIGN.md §8e)
+    raise SystemExit("bench.py: the sharded lasso path is not built in this tree")
 
 
 def main():

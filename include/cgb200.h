@@ -16,8 +16,13 @@
  *     cgb_last_error().  There is no CPU fallback: without a usable
  *     sm_100 device every compute call fails with CGB_ENODEV.
  *   - A cgb_ctx owns the persistent-kernel resources (grid barrier,
- *     reduction banks).  Calls sharing one ctx must be serialised on one
- *     stream; use one ctx per stream for concurrency.
+ *     reduction banks) and the plan temporaries of the operators created
+ *     on it.  Every launching call on a ctx is ordered after the previous
+ *     one: a call on a different stream first makes that stream wait for
+ *     the ctx's last stream (event), and host threads are serialised by a
+ *     ctx mutex.  Calls on one ctx therefore never overlap on the device;
+ *     use one ctx per concurrent solver.  Operators and cones must be used
+ *     with the ctx they were created on (CGB_EINVAL otherwise).
  */
 #ifndef CGB200_H
 #define CGB200_H
@@ -28,7 +33,7 @@
 extern "C" {
 #endif
 
-#define CGB_ABI_VERSION 2
+#define CGB_ABI_VERSION 3
 
 /* ---- error codes --------------------------------------------------------- */
 #define CGB_OK 0
@@ -152,6 +157,7 @@ typedef struct cgb_scs_settings {       /* ScsSettings (scs.py:84-118)          
 } cgb_scs_settings;
 
 typedef struct cgb_scs_problem {
+  int64_t struct_size; /* sizeof(cgb_scs_problem): checked by cgb_scs_run    */
   int64_t n, m;
   const cgb_op* A;
   const cgb_cones* K;
@@ -161,11 +167,11 @@ typedef struct cgb_scs_problem {
   double denom;        /* 1 + h.g                                            */
   double pr_scale;     /* 1 / (1 + ||b||)                                    */
   double dr_scale;     /* 1 / (1 + ||c||)                                    */
-  /* b (c) is exactly zero outside [b_nz_begin, b_nz_end) ([c_nz_begin,
-   * c_nz_end)): the loop skips those loads.  Both 0 (a zero-initialised
-   * struct) = no information: the whole vector is streamed.               */
-  int64_t b_nz_begin, b_nz_end;
-  int64_t c_nz_begin, c_nz_end;
+  /* The loop measures the index ranges outside which b and c are exactly
+   * zero once per call (one device pass) and skips those loads; the
+   * trajectory is bitwise the same as with CGB_SCS_NO_ZERO_SKIP.          */
+  int32_t flags;
+  int32_t reserved;
 } cgb_scs_problem;
 
 /* Device buffers owned by the caller.  N = n + m + 1.
@@ -193,6 +199,8 @@ typedef struct cgb_scs_work {
 #define CGB_ST_GAP 6      /* last computed gap                                */
 #define CGB_ST_LASTCG 7   /* CG iterations of the last splitting iteration    */
 #define CGB_STATE_LEN 16
+
+#define CGB_SCS_NO_ZERO_SKIP 1  /* cgb_scs_problem.flags: stream all of b and c */
 
 /* Run splitting iterations on device until the status latches, k reaches
  * settings->max_iters, or `max_steps` iterations have run in this call.

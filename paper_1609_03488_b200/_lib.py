@@ -14,7 +14,7 @@ import threading
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("CGB200_LIB") or os.path.join(LIB_DIR, "libcgb200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # error codes
 CGB_OK = 0
@@ -65,11 +65,16 @@ class ScsSettingsC(ctypes.Structure):
                 ("cg_eps_factor", _f64), ("cg_max_iter", _i64), ("cert_tau_ratio", _f64)]
 
 
+SCS_NO_ZERO_SKIP = 1
+
+
 class ScsProblemC(ctypes.Structure):
-    _fields_ = [("n", _i64), ("m", _i64), ("A", _vp), ("K", _vp), ("b", _vp), ("c", _vp),
-                ("g", _vp), ("denom", _f64), ("pr_scale", _f64), ("dr_scale", _f64),
-                ("b_nz_begin", _i64), ("b_nz_end", _i64), ("c_nz_begin", _i64),
-                ("c_nz_end", _i64)]
+    _fields_ = [("struct_size", _i64), ("n", _i64), ("m", _i64), ("A", _vp), ("K", _vp),
+                ("b", _vp), ("c", _vp), ("g", _vp), ("denom", _f64), ("pr_scale", _f64),
+                ("dr_scale", _f64), ("flags", _i32), ("reserved", _i32)]
+
+    def __init__(self, **kw):
+        super().__init__(struct_size=ctypes.sizeof(ScsProblemC), **kw)
 
 
 class ScsWorkC(ctypes.Structure):

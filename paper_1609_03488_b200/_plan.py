@@ -376,6 +376,20 @@ def _leaf_data_bytes(leaf: _lib.Leaf, nnz: int) -> int:
     return 0
 
 
+def _leaf_flops(leaf: _lib.Leaf, nnz: int) -> int:
+    """Algorithmic float64 flops (2 per multiply-add) of one leaf application."""
+    k = leaf.kind
+    if k == _lib.LEAF_DENSE:
+        return 2 * leaf.rows * leaf.cols
+    if k == _lib.LEAF_CSR:
+        return 2 * nnz
+    if k in (_lib.LEAF_CONV1D, _lib.LEAF_CORR1D):
+        return 2 * leaf.n0 * leaf.k0          # every signal sample meets every tap once
+    if k in (_lib.LEAF_CONV2D, _lib.LEAF_CORR2D):
+        return 2 * leaf.n0 * leaf.n1 * leaf.k0 * leaf.k1
+    return 0
+
+
 class DeviceOp:
     """Compiled forward + adjoint plans of one expression (a cgb_op)."""
 
@@ -424,6 +438,12 @@ class DeviceOp:
         return {"leaves": len(b.leaves), "terms": getattr(b, "nterms", 0),
                 "rowblocks": getattr(b, "nrowblocks", 0), "levels": getattr(b, "nlevels", 1),
                 "temps": len(b.temp_len)}
+
+    def algo_flops(self, adjoint: bool = False) -> int:
+        """Algorithmic flops of one application (leaf multiply-adds; the
+        alpha-scaled term sums are not counted)."""
+        b = self.adj if adjoint else self.fwd
+        return sum(_leaf_flops(leaf, b.leaf_nnz.get(i, 0)) for i, leaf in enumerate(b.leaves))
 
     def algo_bytes(self, adjoint: bool = False) -> int:
         """Compulsory bytes of one application: operand reads + output write."""

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -718,7 +719,19 @@ struct ScsArgs {
   int resid_every;
   int stash_cap;   // doubles of shared memory per CTA for the SOC stash
   double* prof;    // PROF_N phase times (ns) or null
-  int64_t b_lo, b_hi, c_lo, c_hi;  // b, c are zero outside [lo, hi) (skip those loads)
+  int no_skip;     // 1: stream all of b and c (CGB_SCS_NO_ZERO_SKIP)
+};
+
+// [first, last + 1) of the nonzeros of b (slots 0, 1) and c (slots 2, 3),
+// as maxima of (-first, last + 1) so one max-reduction gives both ends
+struct NzRange {
+  double r0, r1;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[1], int64_t) {
+    if (v[0] != 0.0) {
+      r0 = fmax(r0, -(double)i);
+      r1 = fmax(r1, (double)(i + 1));
+    }
+  }
 };
 
 // CG tolerance exactly as the solver graph computes it (scs.py:290-311)
@@ -869,6 +882,29 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
   const bool use_stash = stash_need <= (int64_t)a.stash_cap;
   double* const stash_base = cgb_dyn_smem;
 
+  // b and c are exactly zero outside [b_lo, b_hi) / [c_lo, c_hi) (stuffed
+  // problems: deconv b = (0, 0, -b_signal), c = (0, 1)); the loop skips those
+  // loads.  The ranges are measured here, once per launch (one pass over b
+  // and c), so no caller-supplied hint can drop a nonzero.
+  int64_t b_lo = 0, b_hi = m, c_lo = 0, c_hi = n;
+  if (!a.no_skip) {
+    double rr[4];
+    {
+      NzRange fb{-DBL_MAX, -DBL_MAX};
+      const double* sb[1] = {a.b};
+      bulk_stream<1>(m, sb, fb);
+      NzRange fc{-DBL_MAX, -DBL_MAX};
+      const double* sc[1] = {a.c};
+      bulk_stream<1>(n, sc, fc);
+      rr[0] = fb.r0; rr[1] = fb.r1; rr[2] = fc.r0; rr[3] = fc.r1;
+    }
+    gs.reduce_max(rr);
+    b_lo = rr[1] > 0.0 ? (int64_t)(-rr[0]) : 0;
+    b_hi = rr[1] > 0.0 ? (int64_t)rr[1] : 0;
+    c_lo = rr[3] > 0.0 ? (int64_t)(-rr[2]) : 0;
+    c_hi = rr[3] > 0.0 ? (int64_t)rr[3] : 0;
+  }
+
   // running scalars: b.(A x) follows x through the CG updates; b.w_y is
   // summed by every cone step for the next subspace step.
   double bax = 0.0, bwy_part = 0.0;
@@ -898,7 +934,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double s[4] = {0.0, 0.0, 0.0, bwy_part};
     {
       InVec in{wy, nullptr, 0.0};
-      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev, a.c_lo, a.c_hi};
+      EpiRhs e{W.w, W.cgx, W.gx, a.c, W.r, wx_stale ? a.g : nullptr, tau_prev, c_lo, c_hi};
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = a.prof + 16;
       apply_plan<TD>(Aj, in, e, s, gs);
       if (a.prof && threadIdx.x == 0) cgb_tl_acc = nullptr;
@@ -911,8 +947,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     double rns = s[1];
     double cx = s[2];
     const double bwy = s[3];
-    CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c, a.b_lo, a.b_hi,
-             a.c_lo, a.c_hi};
+    CgBufs B{W.cgx, W.r, W.p0, nullptr, W.t, W.tax, W.gx, a.b, a.c, b_lo, b_hi, c_lo, c_hi};
     const int64_t cgk = cg_loop<TD>(F, Aj, CGB_RECIPE_NORMAL, 1.0, B, n, m, rns, delta, floor_,
                                 cg_max, gs, &cx, &bax, prof);
     // tau~ = (w_tau + h.p) / (1 + h.g) with h.p = c.p1 + b.(w_y + A p1)
@@ -941,7 +976,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     for (int sg_i = 0; sg_i < K.nseg; ++sg_i) {
       const DevSeg sg = K.seg[sg_i];
       if (sg.kind == SEG_SOC_LARGE) continue;
-      if (sg.end <= a.b_lo || sg.begin >= a.b_hi) {  // b == 0 here: no b.w_y term
+      if (sg.end <= b_lo || sg.begin >= b_hi) {  // b == 0 here: no b.w_y term
         ConeElemNoB f{&cs, sg.begin, sg.kind};
         const double* src[4] = {wy + sg.begin, W.tax + sg.begin, a.g + n + sg.begin,
                                 W.v + n + sg.begin};
@@ -1211,6 +1246,11 @@ struct cgb_ctx {
   double* host_result;
   double* prof;      // k_scs phase accumulator (device, PROF_N doubles) or null
   int grid_override; // CGB_GRID (experiments): fewer CTAs than SMs, 0 = off
+  // launch ordering: every launch on this ctx follows the previous one
+  std::mutex mu;            // host threads
+  cudaStream_t last = nullptr;
+  bool has_last = false;
+  cudaEvent_t order_ev = nullptr;
 };
 
 struct PlanStore {
@@ -1223,9 +1263,11 @@ struct PlanStore {
 
 struct cgb_op {
   PlanStore fwd, adj;
+  const cgb_ctx* ctx = nullptr;
 };
 
 struct cgb_cones {
+  const cgb_ctx* ctx = nullptr;
   DevCones dc{};
   void* blob = nullptr;
   int64_t m = 0;
@@ -1256,12 +1298,26 @@ int grid_for(const cgb_ctx* ctx, K kernel, size_t smem, int* grid) {
   return CGB_OK;
 }
 
+// Order this launch after the ctx's previous one (the grid barrier, the
+// reduction banks and the plan temporaries are per ctx).  Caller holds mu.
+int order_after_last(cgb_ctx* ctx, cudaStream_t stream) {
+  if (ctx->has_last && ctx->last != stream) {
+    CUDA_TRY(cudaEventRecord(ctx->order_ev, ctx->last));
+    CUDA_TRY(cudaStreamWaitEvent(stream, ctx->order_ev, 0));
+  }
+  ctx->last = stream;
+  ctx->has_last = true;
+  return CGB_OK;
+}
+
 template <class K, class A>
-int launch_coop(const cgb_ctx* ctx, K kernel, A& args, size_t smem, cudaStream_t stream) {
+int launch_coop(cgb_ctx* ctx, K kernel, A& args, size_t smem, cudaStream_t stream) {
   int grid = 0;
   int rc = grid_for(ctx, kernel, smem, &grid);
   if (rc) return rc;
   if (grid > CGB_MAXG) return fail(CGB_ECOOP, "grid larger than CGB_MAXG");
+  rc = order_after_last(ctx, stream);
+  if (rc) return rc;
   // the grid barrier counts arrivals from zero in every launch
   CUDA_TRY(cudaMemsetAsync(&ctx->bar->count, 0, sizeof(unsigned long long), stream));
   void* params[] = {&args};
@@ -1605,6 +1661,10 @@ int cgb_ctx_create(int device, cgb_ctx** out) {
   cudaMemset(c->bar, 0, sizeof(GridBar));
   cudaMemset(c->partials, 0, sizeof(double) * 2 * CGB_MAXP * c->max_grid);
   cudaMallocHost(&c->host_result, sizeof(double) * 16);
+  if (cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return fail(CGB_ECUDA, "ctx event creation failed");
+  }
   CUDA_TRY(cudaDeviceSynchronize());
   *out = c;
   return CGB_OK;
@@ -1616,6 +1676,7 @@ int cgb_ctx_destroy(cgb_ctx* ctx) {
   cudaFree(ctx->partials);
   cudaFree(ctx->result);
   cudaFreeHost(ctx->host_result);
+  if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
   delete ctx;
   return CGB_OK;
 }
@@ -1638,6 +1699,7 @@ int cgb_op_create(cgb_ctx* ctx, const cgb_plan_desc* fwd, const cgb_plan_desc* a
   if (!fwd || !adj || fwd->in_len != adj->out_len || fwd->out_len != adj->in_len)
     return fail(CGB_EINVAL, "forward/adjoint plan shapes disagree");
   cgb_op* op = new cgb_op();
+  op->ctx = ctx;
   int rc = build_plan(fwd, &op->fwd);
   if (rc == CGB_OK) rc = build_plan(adj, &op->adj);
   if (rc != CGB_OK) {
@@ -1661,6 +1723,8 @@ int cgb_op_destroy(cgb_op* op) {
 int cgb_op_apply(cgb_ctx* ctx, const cgb_op* op, int adjoint, const double* x, double* y,
                  void* stream) {
   if (!ctx || !op || !x || !y) return fail(CGB_EINVAL, "null argument");
+  if (op->ctx != ctx) return fail(CGB_EINVAL, "operator belongs to another ctx");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   ApplyArgs a{ctx->bar, ctx->partials, adjoint ? op->adj.dp : op->fwd.dp, x, y};
   if (a.P.smem_xs2 > 0) return launch_coop(ctx, k_apply<true>, a, plan_smem(a.P), (cudaStream_t)stream);
   return launch_coop(ctx, k_apply<false>, a, plan_smem(a.P), (cudaStream_t)stream);
@@ -1715,6 +1779,7 @@ int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, in
   CUDA_TRY(cudaMalloc(&dev, blob.host.size() + 256));
   CUDA_TRY(cudaMemcpy(dev, blob.host.data(), blob.host.size(), cudaMemcpyHostToDevice));
   cgb_cones* K = new cgb_cones();
+  K->ctx = ctx;
   K->blob = dev;
   K->m = off;
   K->segs = segs;
@@ -1743,6 +1808,8 @@ int cgb_cones_project(cgb_ctx* ctx, const cgb_cones* K, int dual, const double* 
                       void* stream) {
   if (!ctx || !K || !v || !out) return fail(CGB_EINVAL, "null argument");
   if (v == out) return fail(CGB_EINVAL, "cgb_cones_project: in-place projection not supported");
+  if (K->ctx != ctx) return fail(CGB_EINVAL, "cones belong to another ctx");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   ConeArgs a{ctx->bar, ctx->partials, K->dc, dual, v, out};
   return launch_coop(ctx, k_cones, a, 0, (cudaStream_t)stream);
 }
@@ -1750,10 +1817,12 @@ int cgb_cones_project(cgb_ctx* ctx, const cgb_cones* K, int dual, const double* 
 int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const double* b,
                  double* x, double tol, int64_t max_iter, cgb_cg_result* res, void* stream) {
   if (!ctx || !op || !b || !x || !res) return fail(CGB_EINVAL, "null argument");
+  if (op->ctx != ctx) return fail(CGB_EINVAL, "operator belongs to another ctx");
   if (recipe != CGB_RECIPE_DIRECT && recipe != CGB_RECIPE_NORMAL)
     return fail(CGB_EINVAL, "unknown CG recipe");
   const int64_t n = op->fwd.in_len, m = op->fwd.out_len;
   if (recipe == CGB_RECIPE_DIRECT && n != m) return fail(CGB_EINVAL, "direct CG needs square A");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   cudaStream_t s = (cudaStream_t)stream;
   double* scratch = nullptr;
   CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * (3 * n + m + 1), s));
@@ -1763,13 +1832,17 @@ int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const d
   int rc = (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
                ? launch_coop(ctx, k_cg<true>, a, solver_smem(a.F, a.Aj), s)
                : launch_coop(ctx, k_cg<false>, a, solver_smem(a.F, a.Aj), s);
-  if (rc == CGB_OK) {
-    CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 3 * sizeof(double),
-                             cudaMemcpyDeviceToHost, s));
-  }
-  cudaFreeAsync(scratch, s);
-  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaError_t ce = cudaSuccess;
+  if (rc == CGB_OK)
+    ce = cudaMemcpyAsync(ctx->host_result, ctx->result, 3 * sizeof(double),
+                         cudaMemcpyDeviceToHost, s);
+  // the scratch is released on every path, before any error return
+  const cudaError_t fe = cudaFreeAsync(scratch, s);
+  const cudaError_t se = cudaStreamSynchronize(s);
   if (rc) return rc;
+  if (ce != cudaSuccess) return fail(CGB_ECUDA, std::string("result copy: ") + cudaGetErrorString(ce));
+  if (fe != cudaSuccess) return fail(CGB_ECUDA, std::string("scratch free: ") + cudaGetErrorString(fe));
+  if (se != cudaSuccess) return fail(CGB_ECUDA, std::string("k_cg: ") + cudaGetErrorString(se));
   res->iterations = (int64_t)ctx->host_result[0];
   res->final_residual_norm = std::sqrt(ctx->host_result[1]);
   res->b_norm = std::sqrt(ctx->host_result[2]);
@@ -1782,6 +1855,8 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
                     double* z, double tol, int64_t max_iter, const double* c, const double* b,
                     double* scratch, cgb_cg_result* res, double* hdot, void* stream) {
   if (!ctx || !op || !d1 || !d2 || !z || !scratch) return fail(CGB_EINVAL, "null argument");
+  if (op->ctx != ctx) return fail(CGB_EINVAL, "operator belongs to another ctx");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   const int64_t n = op->fwd.in_len, m = op->fwd.out_len;
   cudaStream_t s = (cudaStream_t)stream;
   InnerArgs a{ctx->bar, ctx->partials, op->fwd.dp, op->adj.dp, d1, d2, z, c, b,
@@ -1807,18 +1882,26 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
 
 int cgb_debug_barrier(cgb_ctx* ctx, int64_t iters, int mode, void* stream) {
   if (!ctx || iters < 0) return fail(CGB_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   BarArgs a{ctx->bar, ctx->partials, iters, mode, ctx->result};
   return launch_coop(ctx, k_barrier, a, 0, (cudaStream_t)stream);
 }
 
 int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_settings* st,
                 cgb_scs_work* work, int64_t max_steps, int resid_every_iter, void* stream) {
-  if (!ctx || !prob || !st || !work || !prob->A || !prob->K)
-    return fail(CGB_EINVAL, "null argument");
+  if (!ctx || !prob || !st || !work) return fail(CGB_EINVAL, "null argument");
+  if (prob->struct_size != (int64_t)sizeof(cgb_scs_problem))
+    return fail(CGB_EINVAL, "cgb_scs_problem.struct_size mismatch (ABI v" +
+                                std::to_string(CGB_ABI_VERSION) + " layout expected)");
+  if (!prob->A || !prob->K || !prob->b || !prob->c || !prob->g)
+    return fail(CGB_EINVAL, "null problem member");
   const cgb_op* op = prob->A;
+  if (op->ctx != ctx || prob->K->ctx != ctx)
+    return fail(CGB_EINVAL, "operator / cones belong to another ctx");
   if (op->fwd.in_len != prob->n || op->fwd.out_len != prob->m || prob->K->m != prob->m)
     return fail(CGB_EINVAL, "problem dimensions disagree with operator / cones");
   if (st->check_interval < 1 || st->eps <= 0) return fail(CGB_EINVAL, "bad settings");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   ScsArgs a;
   a.bar = ctx->bar;
   a.partials = ctx->partials;
@@ -1839,16 +1922,7 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.max_steps = max_steps;
   a.resid_every = resid_every_iter;
   a.prof = ctx->prof;
-  // zero-initialised ranges mean "no information": stream all of b / c
-  const bool bz = prob->b_nz_begin == 0 && prob->b_nz_end == 0;
-  const bool cz = prob->c_nz_begin == 0 && prob->c_nz_end == 0;
-  a.b_lo = bz ? 0 : prob->b_nz_begin;
-  a.b_hi = bz ? prob->m : prob->b_nz_end;
-  a.c_lo = cz ? 0 : prob->c_nz_begin;
-  a.c_hi = cz ? prob->n : prob->c_nz_end;
-  if (a.b_lo < 0 || a.b_hi > prob->m || a.b_lo > a.b_hi || a.c_lo < 0 || a.c_hi > prob->n ||
-      a.c_lo > a.c_hi)
-    return fail(CGB_EINVAL, "cgb_scs_run: b/c nonzero range out of bounds");
+  a.no_skip = (prob->flags & CGB_SCS_NO_ZERO_SKIP) ? 1 : 0;
   // shared memory: conv staging of the plans, or the large-SOC stash of the
   // cone step, whichever is larger (never live together; one CTA per SM --
   // the kernel re-checks the stash need with the real grid)

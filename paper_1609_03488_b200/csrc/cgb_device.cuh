@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <float.h>
 #include <stdint.h>
 
 #include "../../include/cgb200.h"
@@ -330,6 +331,45 @@ struct GridSync {
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < NP; ++p) v[p] = red_out[p];
+    bank ^= 1;
+  }
+
+  // Max of v[0..NP) over every thread of the grid (same structure as
+  // reduce; max is order independent, so the result is exact).
+  template <int NP>
+  __device__ void reduce_max(double (&v)[NP]) {
+    static_assert(NP <= CGB_MAXP && NP <= CGB_WARPS, "too many reduction slots");
+    __shared__ double rmx_smem[CGB_WARPS][CGB_MAXP];
+    __shared__ double rmx_out[CGB_MAXP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      double s = v[p];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+      if (lane == 0) rmx_smem[wid][p] = s;
+    }
+    __syncthreads();
+    const int G = gridDim.x;
+    double* bankp = partials + (size_t)bank * CGB_MAXP * G;
+    if (wid < NP) {
+      double s = lane < CGB_WARPS ? rmx_smem[lane][wid] : -DBL_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+      if (lane == 0) bankp[(size_t)wid * G + blockIdx.x] = s;
+    }
+    sync();
+    if (wid < NP) {
+      const double* src = bankp + (size_t)wid * G;
+      double s = -DBL_MAX;
+      for (int i = lane; i < G; i += 32) s = fmax(s, __ldcg(src + i));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+      if (lane == 0) rmx_out[wid] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < NP; ++p) v[p] = rmx_out[p];
     bank ^= 1;
   }
 };

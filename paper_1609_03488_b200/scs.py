@@ -279,14 +279,15 @@ class SolverPlan:
         self.buf["state"] = torch.zeros(_lib.STATE_LEN, **f64)
         self.work = _lib.ScsWorkC(**{nm: t.data_ptr() for nm, t in self.buf.items()})
         ca = self.cached
-        bl, bh = _nonzero_range(problem.b)
-        cl, ch = _nonzero_range(problem.c)
+        # the loop skips the loads of b and c outside their nonzero ranges
+        # (it measures them itself); the host copy is for bytes_model only
+        self.b_nz = _nonzero_range(problem.b)
+        self.c_nz = _nonzero_range(problem.c)
         self.cprob = _lib.ScsProblemC(
             n=n, m=m, A=self.dev.handle.value, K=self.cones.handle.value,
             b=ca.b_device.data_ptr(), c=ca.c_device.data_ptr(), g=ca.g_device.data_ptr(),
             denom=ca.denom, pr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.b))),
-            dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))),
-            b_nz_begin=bl, b_nz_end=bh, c_nz_begin=cl, c_nz_end=ch)
+            dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))))
         self.csettings = settings.to_c(n)
         self.reset()
 
@@ -371,11 +372,21 @@ class SolverPlan:
         per_check = fr + ar + W * (3 * n + 4 * m)  # A u_x, A^T u_y, c.u_x, b.u_y
         # the loop skips b / c where they are zero (cgb_scs_problem.*_nz_*):
         # the rhs c read and the tracked c.p / b.t dots stream only the range
-        cz = n - (self.cprob.c_nz_end - self.cprob.c_nz_begin)
-        bz = m - (self.cprob.b_nz_end - self.cprob.b_nz_begin)
+        skip = not (self.cprob.flags & _lib.SCS_NO_ZERO_SKIP)
+        cz = n - (self.c_nz[1] - self.c_nz[0]) if skip else 0
+        bz = m - (self.b_nz[1] - self.b_nz[0]) if skip else 0
         per_iter -= W * cz
         per_cg -= W * (cz + bz)
         return {"per_iter": per_iter, "per_cg_iter": per_cg, "per_check": per_check}
+
+    def launch_flops(self, iterations: int, cg_total: int) -> int:
+        """Algorithmic operator flops of one k_scs launch: one adjoint apply
+        per iteration (rhs), a forward and an adjoint per CG step, both per
+        residual check (the FP64 side of the roofline; the stream passes'
+        few flops per element are not counted)."""
+        ff, fa = self.dev.algo_flops(False), self.dev.algo_flops(True)
+        checks = iterations // max(1, self.settings.check_interval)
+        return iterations * fa + cg_total * (ff + fa) + checks * (ff + fa)
 
     def launch_bytes(self, iterations: int, cg_total: int) -> int:
         """Algorithmic bytes of one k_scs launch that ran ``iterations``

@@ -43,6 +43,8 @@ def build_tree(t: dict, arrays, ns):
         return ns.SparseMatrix(mat)
     if k == "Conv1D":
         return ns.Conv1D(np.array(arrays[t["kernel"]]), t["n"])
+    if k == "Conv2D":
+        return ns.Conv2D(np.array(arrays[t["kernel"]]), tuple(t["image_shape"]))
     if k == "Identity":
         return ns.Identity(t["n"])
     if k == "ZeroOp":

@@ -1,0 +1,244 @@
+"""Rounding envelopes of BENCH-FAMILY instances (the BASELINE.json configs
+and CPU-feasible members of their families), measured on the CPU with the
+real reference (conegraph, /root/reference) where it supports the problem,
+else with the pinned numpy oracle (oracle/scs_ref.py) -- 2-d convolution
+and exponential cones are north-star extensions the reference lacks.
+
+Why envelopes: the splitting solver with a warm-started inexact CG step
+amplifies rounding (tests/golden/make_envelopes.py shows it on the golden
+cases), so the iteration at which the status latches is a distribution
+over last-bit perturbations of the data.  For every instance this script
+solves the unperturbed problem and R copies with b, c multiplied
+elementwise by (1 + U(-4, 4) ulp), and appends one JSON line per solve to
+tests/golden/bench_envelopes.jsonl (committed).  The GPU tests
+(tests/test_gpu_envelopes.py) rebuild the same instance from the same
+generator and require:
+  * zero-spread envelope  -> the device count equals it exactly and pobj
+    agrees to 1e-6 relative;
+  * otherwise             -> the device count lies in [min - CI, max + CI]
+    (CI = check_interval) and pobj inside the envelope's pobj range
+    widened by its own spread.
+
+Instances are the bench.py workload generators (host-only numpy) at the
+sizes named here; the stuffed expression tree is serialized from the
+product's host-side builders and rebuilt with the reference's (or the
+oracle's) own expression classes, so every solver sees identical data.
+
+usage (build container, background):
+    python tests/golden/make_bench_envelopes.py [instance ...]
+        ENVELOPE_SEEDS=8 ENVELOPE_WORKERS=6
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+import types
+from concurrent.futures import ProcessPoolExecutor, as_completed
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+for p in (ROOT, os.path.dirname(HERE)):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+OUT = os.path.join(HERE, "bench_envelopes.jsonl")
+ULP = np.finfo(np.float64).eps
+EPS = 1e-3
+MAX_ITERS = 100_000
+
+# name -> (workload constructor spec, solver, seeds); cheap instances first
+INSTANCES = {
+    # configs[0] at its full size
+    "lasso_dense_1000x500": ({"workload": "lasso_dense"}, "reference", 16),
+    # configs[4] families at CPU-feasible sizes
+    "soc_ls_20000x200": ({"workload": "soc_ls", "m": 20_000, "n": 200}, "reference", 8),
+    "logreg_600x20": ({"workload": "logreg", "m": 600, "n": 20}, "oracle", 8),
+    # configs[3] family (CSR lasso, ~80 nnz per column) at a CPU-feasible size
+    "lasso_sparse_80000x10000": ({"workload": "lasso_sparse", "m": 80_000, "n": 10_000,
+                                  "density": 1e-3}, "reference", 8),
+    # configs[2] family (15 x 15 blur) at a CPU-feasible size
+    "deconv2d_256_k15": ({"workload": "deconv2d", "h": 256, "w": 256, "k": 15}, "oracle", 8),
+    # configs[1] family (kernel 101) at a CPU-feasible size, and the bench instance itself
+    "deconv1d_n100000_k101": ({"workload": "deconv1d", "n": 100_000}, "reference", 8),
+    "deconv1d_n1000000_k101": ({"workload": "deconv1d", "n": 1_000_000}, "oracle", 4),
+}
+
+
+def workload(spec: dict):
+    """The bench.py generator of an instance (host numpy, product builders)."""
+    import bench
+    w = spec["workload"]
+    if w == "deconv1d":
+        return bench.Deconv1D(spec["n"])
+    if w == "deconv2d":
+        return bench.Deconv2D(spec["h"], spec["w"], spec["k"])
+    if w == "lasso_dense":
+        return bench.LassoDense()
+    if w == "lasso_sparse":
+        return bench.LassoSparse(spec["m"], spec["n"], spec["density"])
+    if w == "soc_ls":
+        return bench.SocLs(spec["m"], spec["n"])
+    if w == "logreg":
+        return bench.LogReg(spec["m"], spec["n"])
+    raise ValueError(w)
+
+
+def serialize(expr, arrays: dict) -> dict:
+    """Product expression tree -> the dict form tests/_golden.build_tree reads."""
+    k = type(expr).__name__
+
+    def arr(a):
+        key = f"a{len(arrays)}"
+        arrays[key] = np.asarray(a)
+        return key
+
+    if k == "DenseMatrix":
+        if expr._transpose_of is not None:
+            return {"k": "AdjointOf", "child": serialize(expr._transpose_of, arrays)}
+        return {"k": k, "values": arr(expr.values)}
+    if k == "SparseMatrix":
+        if expr._transpose_of is not None:
+            return {"k": "AdjointOf", "child": serialize(expr._transpose_of, arrays)}
+        m = expr.matrix
+        return {"k": k, "data": arr(m.data), "indices": arr(m.indices),
+                "indptr": arr(m.indptr), "m": m.shape[0], "n": m.shape[1]}
+    if k == "Conv1D":
+        return {"k": k, "kernel": arr(expr.kernel), "n": expr.n}
+    if k == "Conv2D":
+        return {"k": k, "kernel": arr(expr.kernel), "image_shape": list(expr.image_shape)}
+    if k == "Identity":
+        return {"k": k, "n": expr.rows}
+    if k == "ZeroOp":
+        return {"k": k, "m": expr.rows, "n": expr.cols}
+    if k == "Scale":
+        return {"k": k, "alpha": float(expr.alpha), "child": serialize(expr.child, arrays)}
+    if k in ("Sum", "Compose"):
+        return {"k": k, "left": serialize(expr.left, arrays),
+                "right": serialize(expr.right, arrays)}
+    if k == "VStack":
+        return {"k": k, "children": [serialize(c, arrays) for c in expr.children]}
+    if k == "AdjointOf":
+        return {"k": k, "child": serialize(expr.child, arrays)}
+    raise TypeError(k)
+
+
+def instance_data(name: str):
+    spec, solver, _ = INSTANCES[name]
+    prob = workload(spec).problem()
+    arrays: dict = {}
+    tree = serialize(prob.A.expr, arrays)
+    cones = [[type(f).__name__, int(f.dim)] for f in prob.K.factors]
+    return tree, arrays, cones, np.asarray(prob.b), np.asarray(prob.c), solver
+
+
+def b_digest(b: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(b, dtype=np.float64).tobytes()).hexdigest()[:16]
+
+
+def perturb(v: np.ndarray, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(1000 + seed)
+    return v * (1.0 + 4 * ULP * rng.uniform(-1, 1, v.shape))
+
+
+def _solve_job(name: str, seed: int) -> dict:
+    """seed < 0: unperturbed.  Runs in a worker process (1 BLAS thread)."""
+    from _golden import build_cones, build_tree
+    tree, arrays, cones, b, c, solver = instance_data(name)
+    digest = b_digest(b)
+    if seed >= 0:
+        rng_b = perturb(b, seed)
+        c = c * (1.0 + 4 * ULP * np.random.default_rng(2000 + seed).uniform(-1, 1, c.shape))
+        b = rng_b
+    t0 = time.time()
+    if solver == "reference":
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from conegraph import cones as rcones
+        from conegraph import linop as rlinop
+        from conegraph.scs import ConeProblem, ScsSettings, solve
+        ns = types.SimpleNamespace(**{k: getattr(rlinop, k) for k in dir(rlinop)})
+        A = rlinop.Operator(build_tree(tree, arrays, ns))
+        K = rcones.ConeProduct(build_cones(cones, rcones))
+        sol = solve(ConeProblem(A, b, c, K), ScsSettings(eps=EPS, max_iters=MAX_ITERS))
+    else:
+        import _exprs
+        from oracle import scs_ref
+
+        class P:
+            pass
+        p = P()
+        p.A = build_tree(tree, arrays, _exprs)
+        p.b, p.c = b, c
+        p.K = _exprs.ConeProduct(build_cones(cones, _exprs))
+        sol, _ = scs_ref.scs_solve(p, scs_ref.ScsOracleSettings(eps=EPS, max_iters=MAX_ITERS))
+    return {"instance": name, "solver": solver, "seed": seed, "b_digest": digest,
+            "status": sol.status, "iterations": int(sol.iterations), "pobj": float(sol.pobj),
+            "dobj": float(sol.dobj), "avg_cg": float(sol.avg_cg_iterations),
+            "seconds": time.time() - t0,
+            "perturbation": "none" if seed < 0 else "b, c *= 1 + U(-4, 4) ulp"}
+
+
+def _worker_init():
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+
+def done_jobs() -> set:
+    out = set()
+    if os.path.exists(OUT):
+        for line in open(OUT):
+            if line.strip():
+                r = json.loads(line)
+                out.add((r["instance"], r["seed"]))
+    return out
+
+
+def main(names=None):
+    seeds = int(os.environ.get("ENVELOPE_SEEDS", "8"))
+    workers = int(os.environ.get("ENVELOPE_WORKERS", "6"))
+    names = names or list(INSTANCES)
+    have = done_jobs()
+    jobs = [(nm, s) for nm in names for s in range(-1, min(seeds, INSTANCES[nm][2]))
+            if (nm, s) not in have]
+    print(f"{len(jobs)} solves to run on {workers} workers", flush=True)
+    with ProcessPoolExecutor(max_workers=workers, initializer=_worker_init) as ex:
+        futs = {ex.submit(_solve_job, nm, s): (nm, s) for nm, s in jobs}
+        for f in as_completed(futs):
+            nm, s = futs[f]
+            try:
+                r = f.result()
+            except Exception as exc:  # noqa: BLE001
+                print(f"{nm} seed {s}: FAILED {exc!r}", flush=True)
+                continue
+            with open(OUT, "a") as fh:
+                fh.write(json.dumps(r, sort_keys=True) + "\n")
+            print(f"{nm} seed {s}: {r['status']} {r['iterations']} it pobj {r['pobj']:.10g} "
+                  f"({r['seconds']:.0f} s)", flush=True)
+
+
+def load_envelopes(path: str = OUT) -> dict:
+    """instance -> {"unperturbed": rec | None, "perturbed": [rec...]}"""
+    env: dict = {}
+    if not os.path.exists(path):
+        return env
+    for line in open(path):
+        if not line.strip():
+            continue
+        r = json.loads(line)
+        e = env.setdefault(r["instance"], {"unperturbed": None, "perturbed": []})
+        if r["seed"] < 0:
+            e["unperturbed"] = r
+        else:
+            e["perturbed"].append(r)
+    return env
+
+
+if __name__ == "__main__":
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    main(sys.argv[1:] or None)

@@ -8,6 +8,7 @@ check interval for short runs), objective within 1e-6 relative at
 convergence, residuals <= eps.
 """
 
+import ctypes
 import json
 
 import numpy as np
@@ -465,27 +466,80 @@ def test_kron_lowering_matches_numpy():
 
 
 def test_zero_range_skipping_is_bitwise_neutral():
-    """Skipping b / c loads over their zero ranges (cgb_scs_problem
-    b_nz_* / c_nz_*) must not change a single bit of the trajectory: the
-    same plan run with the ranges zeroed (stream everything) ends in the
-    identical state, and out-of-bounds ranges are rejected."""
+    """Skipping b / c loads over their zero ranges (measured on device once
+    per launch) must not change a single bit of the trajectory: the same
+    plan run with CGB_SCS_NO_ZERO_SKIP (stream everything) ends in the
+    identical state; a wrong struct_size is rejected."""
     from paper_1609_03488_b200 import _lib, canon
     n, k = 20_000, 101
     c, b, _ = canon.gen_deconv1d(n, k, seed=5, spikes=20)
     prob = canon.build_deconv(canon.DeconvProblem(c, b, n=n))
     plan = scs.build_scs_graph(prob, scs.ScsSettings(eps=1e-3, max_iters=5000))
     cp = plan.cprob
-    assert (cp.b_nz_begin, cp.c_nz_begin, cp.c_nz_end) == (n + 1, n, n + 1)
+    assert (plan.b_nz[0], plan.c_nz) == (n + 1, (n, n + 1))
     plan.reset()
     plan.run(300)
     skipped = plan.state().copy()
-    saved = (cp.b_nz_begin, cp.b_nz_end, cp.c_nz_begin, cp.c_nz_end)
-    cp.b_nz_begin = cp.b_nz_end = cp.c_nz_begin = cp.c_nz_end = 0
+    u_skip = plan.buf["u"].cpu().numpy()
+    cp.flags = _lib.SCS_NO_ZERO_SKIP
     plan.reset()
     plan.run(300)
     full = plan.state().copy()
     assert np.array_equal(skipped, full)
-    cp.b_nz_begin, cp.b_nz_end = 5, prob.A.rows + 1
+    assert np.array_equal(u_skip, plan.buf["u"].cpu().numpy())
+    cp.flags = 0
+    cp.struct_size = 8
     with pytest.raises(_lib.CgbError):
         plan.run(1)
-    cp.b_nz_begin, cp.b_nz_end, cp.c_nz_begin, cp.c_nz_end = saved
+    cp.struct_size = ctypes.sizeof(_lib.ScsProblemC)
+
+
+def test_calls_on_two_streams_are_ordered():
+    """one cgb_ctx (grid barrier, reduction banks, plan
+    temporaries) serves every caller; launches on a second stream are
+    ordered after the ctx's previous stream, so two solves issued back to
+    back on different streams give the sequential results bit for bit."""
+    import torch
+    from paper_1609_03488_b200 import canon
+    n, k = 20_000, 101
+    c, b, _ = canon.gen_deconv1d(n, k, seed=3, spikes=20)
+    prob = canon.build_deconv(canon.DeconvProblem(c, b, n=n))
+    st = scs.ScsSettings(eps=1e-3, max_iters=400)
+    p1 = scs.build_scs_graph(prob, st)
+    p2 = scs.build_scs_graph(prob, st)
+    p1.reset()
+    p1.run(400)
+    ref = p1.state().copy()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    p1.reset()
+    p2.reset()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        p1.run(400)
+    with torch.cuda.stream(s2):
+        p2.run(400)
+    torch.cuda.synchronize()
+    assert np.array_equal(p1.state(), ref)
+    assert np.array_equal(p2.state(), ref)
+
+
+def test_tracked_products_do_not_drift():
+    """ADVICE r1: the loop never recomputes A cgx (tax) or A^T A cgx (gx);
+    they follow cgx through every CG update.  After a long run they must
+    still equal fresh operator applications to ~1e-12 relative."""
+    from paper_1609_03488_b200 import canon
+    n, k = 20_000, 101
+    c, b, _ = canon.gen_deconv1d(n, k, seed=5, spikes=20)
+    prob = canon.build_deconv(canon.DeconvProblem(c, b, n=n))
+    plan = scs.build_scs_graph(prob, scs.ScsSettings(eps=1e-6, max_iters=6000))
+    plan.reset()
+    plan.run(6000)
+    st = plan.state()
+    assert st[3] > 500, "the run should take many CG steps"
+    x = plan.buf["cgx"]
+    ax = plan.dev.apply(x)
+    gx = plan.dev.apply(ax, adjoint=True)
+    tax, tgx = plan.buf["tax"], plan.buf["gx"]
+    rel_a = float((ax - tax).norm() / ax.norm())
+    rel_g = float((gx - tgx).norm() / gx.norm())
+    assert rel_a < 1e-12 and rel_g < 1e-12, (rel_a, rel_g)

@@ -140,9 +140,9 @@ def test_logreg_stuffing_permutation_is_a_bijection():
 
 
 def test_nonzero_ranges_of_stuffed_vectors():
-    """The b / c nonzero ranges the loop uses to skip loads
-    (cgb_scs_problem.b_nz_* / c_nz_*): exact first/last nonzero, (0, 0) for
-    an all-zero vector (= "no information" at the ABI: stream everything)."""
+    """The b / c nonzero ranges of the stuffed vectors (the loop measures
+    them on device and skips loads outside; the host copy feeds
+    SolverPlan.bytes_model): exact first/last nonzero, (0, 0) when zero."""
     from paper_1609_03488_b200 import canon, scs
     assert scs._nonzero_range(np.zeros(5)) == (0, 0)
     assert scs._nonzero_range(np.array([0.0, 0.0, 3.0, 0.0, -1.0, 0.0])) == (2, 5)
@@ -157,11 +157,56 @@ def test_nonzero_ranges_of_stuffed_vectors():
     assert scs._nonzero_range(prob.c) == (n, n + 1)
 
 
-def test_abi_problem_struct_carries_ranges():
+def test_abi_problem_struct_layout():
+    """ABI v3: cgb_scs_problem starts with struct_size (checked by the
+    library) and carries flags instead of caller-supplied b/c ranges."""
     from paper_1609_03488_b200 import _lib
     names = [f[0] for f in _lib.ScsProblemC._fields_]
-    assert names[-4:] == ["b_nz_begin", "b_nz_end", "c_nz_begin", "c_nz_end"]
-    assert ctypes.sizeof(_lib.ScsProblemC) == 8 * 2 + 8 * 5 + 8 * 3 + 8 * 4
+    assert names[0] == "struct_size" and names[-2:] == ["flags", "reserved"]
+    assert ctypes.sizeof(_lib.ScsProblemC) == 8 * 3 + 8 * 5 + 8 * 3 + 4 * 2
+    assert _lib.ScsProblemC().struct_size == ctypes.sizeof(_lib.ScsProblemC)
     hdr = open(os.path.join(ROOT, "include", "cgb200.h")).read()
-    for nm in names[-4:]:
+    for nm in names:
         assert nm in hdr
+    assert "b_nz_begin" not in hdr
+    assert f"#define CGB_ABI_VERSION {_lib.ABI_VERSION}" in hdr
+
+
+def test_bench_generators_match_canon():
+    """bench.py restates the data generators so the reference arm imports
+    nothing of the product; they must equal canon's bit for bit."""
+    import bench
+    from paper_1609_03488_b200 import canon
+    for n in (7, 101):
+        assert np.array_equal(bench.gaussian_kernel(n), canon.gaussian_kernel(n))
+    assert np.array_equal(bench.gaussian_kernel2d(15, 15), canon.gaussian_kernel2d(15, 15))
+    a1, y1, w1 = bench.gen_logreg(50, 7, seed=3)
+    a2, y2, w2 = canon.gen_logreg(50, 7, seed=3)
+    assert np.array_equal(a1, a2) and np.array_equal(y1, y2) and np.array_equal(w1, w2)
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("deconv2d", {"h": 16, "w": 21, "k": 3}),
+    ("deconv1d", {"n": 40}),
+    ("lasso_dense", {"m": 30, "n": 12}),
+    ("lasso_sparse", {"m": 300, "n": 40, "density": 0.05}),
+    ("logreg", {"m": 20, "n": 5}),
+    ("soc_ls", {"m": 30, "n": 6}),
+])
+def test_oracle_stuffing_matches_product(name, kw):
+    """oracle/canon_ref.py (reference arm) and the product's canon builders
+    stuff the same problem: identical b, c, cone dims and operator applies."""
+    import bench
+    from oracle import linop_ref
+    wl = bench.WORKLOADS[name](**kw) if name != "deconv1d" else bench.Deconv1D(kw["n"])
+    if name == "deconv1d":
+        c, _, _ = wl.data()
+    pp, po = wl.problem(), wl.oracle_problem()
+    assert np.array_equal(pp.b, po.b) and np.array_equal(pp.c, po.c)
+    assert [(type(f).__name__, f.dim) for f in pp.K.factors] == \
+        [(type(f).__name__, f.dim) for f in po.K.factors]
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(pp.A.cols)
+    y = rng.standard_normal(pp.A.rows)
+    np.testing.assert_array_equal(linop_ref.forward(pp.A.expr, x), linop_ref.forward(po.A, x))
+    np.testing.assert_array_equal(linop_ref.adjoint(pp.A.expr, y), linop_ref.adjoint(po.A, y))
