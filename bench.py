@@ -410,6 +410,8 @@ def _args():
     ap.add_argument("--n", type=int, default=N_SIGNAL, help="deconv1d signal length")
     ap.add_argument("--step-iters", type=int, default=-1,
                     help="splitting iterations per step (0 = to eps; default per workload)")
+    ap.add_argument("--shards", type=int, default=1,
+                    help="lasso_sparse on one GPU: ranks of the sharded solver sharing it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-solve", action="store_true",
@@ -621,7 +623,7 @@ def run_b200(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.workload == "lasso_sparse" and world > 1:
+    if args.workload == "lasso_sparse" and (world > 1 or args.shards > 1):
         return run_b200_sharded(args)
     from paper_1609_03488_b200 import _lib, scs
 
@@ -800,9 +802,116 @@ def run_b200(args) -> None:
 
 
 def run_b200_sharded(args) -> None:
-    """configs[3] row-sharded over the ranks (see shard.py)."""
-    from paper_1609_03488_b200 import shard  # noqa: F401  (built in DESIGN.md §8e)
-    raise SystemExit("bench.py: the sharded lasso path is not built in this tree")
+    """configs[3] row-sharded (paper_1609_03488_b200/shard.py).
+
+    Under torchrun: one rank per GPU, peer buffers mapped by CUDA IPC, the
+    whole job is ONE solve (strong scaling): value = iterations / max over
+    ranks of the device time.  With --shards R on a single process: R ranks
+    sharing this GPU (each 1/R of the SMs) -- the sharded kernel's cost,
+    not a scaling number."""
+    import torch
+    from paper_1609_03488_b200 import _lib, scs, shard
+
+    world, rank, local = _dist()
+    wl = make_workload(args)
+    S = _step_iters(args, wl)
+    cap = S if S > 0 else MAX_ITERS
+    settings = scs.ScsSettings(eps=wl.eps, max_iters=MAX_ITERS)
+    prob = wl.problem()
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    if world > 1:
+        lay = shard.layout_for(prob, world, rank)
+        rs = shard.RankSolver(prob, settings, lay, local, ipc=True)
+        shard.connect_ipc(rs)
+        ranks = [rs]
+        parallelism = f"row-sharded over {world} GPUs (NVLink peer memory)"
+
+        def launch(mode, steps):
+            rs.launch(mode, steps, stream)
+    else:
+        grp = shard.ShardGroup(prob, settings, world=args.shards)
+        ranks = grp.ranks
+        parallelism = (f"row-sharded: {args.shards} ranks sharing one GPU "
+                       f"({grp.ranks[0].ctx.geometry()[0] // args.shards} SMs each)")
+
+        def launch(mode, steps):
+            grp._all(mode, steps)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one_step(max_steps):
+        for r in ranks:
+            r.reset()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev[0].record(stream)
+        launch(0, 0)
+        launch(1, max_steps)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        st = ranks[0].state()
+        return ev[0].elapsed_time(ev[1]) / 1e3, int(st[_lib.ST_K]), int(st[_lib.ST_CGT]), \
+            float(st[_lib.ST_STATUS])
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        one_step(cap)
+    results = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            results.append(one_step(cap))
+    tot = sum(r[0] for r in results)
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot = float(t.item())
+    iters = sum(r[1] for r in results)     # one solve for the whole job: not summed
+    value = iters / tot
+    e2e = None
+    if not args.no_e2e and world > 1:
+        e2e_t = []
+        for step in range(1 + args.steps):
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            t1 = time.perf_counter()
+            sol, rsx = shard.solve_sharded(wl.problem(), scs.ScsSettings(eps=wl.eps,
+                                                                         max_iters=cap))
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+            it = int(rsx.state()[_lib.ST_K])
+            rsx.close()
+            if step >= 1:
+                e2e_t.append((float(dt.item()), it))
+        e2e = {"value": sum(i for _, i in e2e_t) / sum(t for t, _ in e2e_t), "unit": "iter/s",
+               "h2d_bytes_per_step": wl.h2d_bytes(),
+               "d2h_bytes_per_step": 8 * (2 * prob.A.rows + prob.A.cols),
+               "ms_per_step": 1e3 * sum(t for t, _ in e2e_t) / len(e2e_t)}
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(results),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config(wl, world, S, parallelism),
+        "iterations_per_step": results[0][1],
+        "avg_cg_iterations": results[0][2] / max(1, results[0][1]),
+        "status": sorted({r[3] for r in results}), "graph_build_s": build_s,
+        "ranks": [{"rows": [r.lay.y0, r.lay.y1], "x_slice": [r.lay.x0, r.lay.x1]}
+                  for r in ranks] if world == 1 else None,
+        "e2e": e2e, "cpu_baseline": None,
+        "gpu_launches": 2 * args.steps * (args.shards if world == 1 else 1),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
 
 
 def main():

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define CGB_ABI_VERSION 3
+#define CGB_ABI_VERSION 4
 
 /* ---- error codes --------------------------------------------------------- */
 #define CGB_OK 0
@@ -198,6 +198,11 @@ typedef struct cgb_scs_work {
 #define CGB_ST_DR 5       /* last computed dual residual                      */
 #define CGB_ST_GAP 6      /* last computed gap                                */
 #define CGB_ST_LASTCG 7   /* CG iterations of the last splitting iteration    */
+#define CGB_ST_TAU 8       /* shard solver: u_tau                               */
+#define CGB_ST_KAPPA 9     /* shard solver: v_tau (kappa)                       */
+#define CGB_ST_DENOM 10    /* shard solver: 1 + h.g of the setup solve          */
+#define CGB_ST_EPOCH 11    /* shard solver: world synchronisations so far       */
+#define CGB_ST_SETUP_CG 12 /* shard solver: CG iterations of the setup solve    */
 #define CGB_STATE_LEN 16
 
 #define CGB_SCS_NO_ZERO_SKIP 1  /* cgb_scs_problem.flags: stream all of b and c */
@@ -231,6 +236,87 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
  * two grid barriers per iteration to separate the cone sub-phases.  NULL
  * disables. */
 int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc);
+
+/* ---- row-sharded solver (one rank per GPU) ------------------
+ * The stuffed operator's rows are split into contiguous ranges, one per
+ * rank; x-space vectors are split into contiguous slices.  Each rank runs
+ * one persistent kernel; ranks exchange data only through peer memory:
+ * A^T partial products are stored straight into the inbox of the rank
+ * owning those columns (reduce-scatter in the adjoint's epilogue), the CG
+ * residual is stored into every rank's full-length x copy (all-gather),
+ * and dot products meet in per-rank mailboxes.  Replaces, for a problem
+ * whose A is too large for one GPU, the same calls as cgb_inner_solve +
+ * cgb_scs_run (scs.py:170-196, 314-413); the reference itself has no
+ * sharding (the decomposition is restated in oracle/shard_ref.py). */
+#define CGB_MAX_RANKS 8
+#define CGB_MBOX_STRIDE 24  /* doubles per mailbox slot (16 values, sequence, pad) */
+
+typedef struct cgb_shard_comm {
+  int32_t world, rank;
+  int64_t x_begin[CGB_MAX_RANKS + 1];  /* x slices: rank q owns [x_begin[q], x_begin[q+1]) */
+  /* device pointers valid on THIS rank's device (peer-mapped):           */
+  double* inbox[CGB_MAX_RANKS];  /* rank q's inbox: world x len_q doubles   */
+  double* xfull[CGB_MAX_RANKS];  /* rank q's full-length x copy: n doubles  */
+  double* mbox[CGB_MAX_RANKS];   /* rank q's mailbox: 2*CGB_MAX_RANKS*CGB_MBOX_STRIDE
+                                    doubles, zeroed before the first call   */
+} cgb_shard_comm;
+
+typedef struct cgb_shard_problem {
+  int64_t struct_size;  /* sizeof(cgb_shard_problem)                        */
+  int64_t n;            /* global x-space length                            */
+  int64_t m;            /* this rank's rows                                 */
+  const cgb_op* A;      /* this rank's rows of A: forward n -> m            */
+  const cgb_cones* K;   /* this rank's cone pieces (cgb_shard_cones_create) */
+  const double* b;      /* m : this rank's rows of b                        */
+  const double* c;      /* this rank's x slice of c                         */
+  double pr_scale;      /* 1 / (1 + ||b||), global                          */
+  double dr_scale;      /* 1 / (1 + ||c||), global                          */
+  double setup_tol;     /* setup CG tolerance (ScsSettings.setup_cg_tol)    */
+} cgb_shard_problem;
+
+typedef struct cgb_shard_work {
+  /* x slice (x_begin[rank+1] - x_begin[rank] doubles each) */
+  double* cgx;   /* CG warm start p1                                        */
+  double* gx;    /* A^T A cgx, tracked                                      */
+  double* p;     /* CG direction                                            */
+  double* wx;    /* w_x = u_x                                               */
+  double* gxs;   /* g_x of the setup solve                                  */
+  /* rows (m doubles each) */
+  double* wy; double* vy; double* uy;
+  double* tax;   /* A cgx, tracked                                          */
+  double* t;     /* CG scratch                                              */
+  double* gy;    /* g_y of the setup solve                                  */
+  double* state; /* CGB_STATE_LEN; TAU = KAPPA = 1 and the rest 0 at start  */
+} cgb_shard_work;
+
+/* This rank's cone pieces.  Piece i covers local rows [begin[i], end[i])
+ * of cone kind kinds[i]; a SOC cut by a rank boundary (or longer than the
+ * single-GPU small-SOC limit) is world-reduced: soc_id[i] in [0, nsoc) is
+ * its index in the global list of such cones (-1 otherwise) and
+ * has_head[i] says whether its head entry is on this rank.  Exponential
+ * cones and small SOCs must not be cut. */
+int cgb_shard_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* begin,
+                           const int64_t* end, const int32_t* soc_id, const int32_t* has_head,
+                           int32_t npieces, int64_t m, int32_t nsoc, cgb_cones** out);
+/* mode 0: the setup solve (g, denom into work / state); mode 1: up to
+ * max_steps splitting iterations.  Every rank must make the same sequence
+ * of calls; each launch is asynchronous on `stream`.  max_steps < 0 only
+ * validates the arguments (a caller launching several ranks checks them
+ * all first: a rank that launched alone would wait for its peers). */
+int cgb_shard_run(cgb_ctx* ctx, const cgb_shard_problem* prob, const cgb_scs_settings* st,
+                  const cgb_shard_comm* comm, cgb_shard_work* work, int mode,
+                  int64_t max_steps, void* stream);
+
+/* Persistent-kernel grid of a ctx: 0 = one CTA per SM (default); g > 0
+ * uses g CTAs, e.g. two ranks sharing one device in tests. */
+int cgb_ctx_set_grid(cgb_ctx* ctx, int32_t grid);
+
+/* Peer memory across processes: a cudaMalloc'd buffer and its 64-byte
+ * CUDA IPC handle; open maps a peer's handle on the current device. */
+int cgb_ipc_alloc(int device, int64_t bytes, void** ptr, void* handle64);
+int cgb_ipc_open(int device, const void* handle64, void** ptr);
+int cgb_ipc_close(void* ptr);
+int cgb_ipc_free(void* ptr);
 
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Run `iters` grid barriers (mode 0) or grid reductions (mode 1) in one

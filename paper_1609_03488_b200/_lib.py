@@ -14,7 +14,7 @@ import threading
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.environ.get("CGB200_LIB") or os.path.join(LIB_DIR, "libcgb200.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # error codes
 CGB_OK = 0
@@ -26,6 +26,9 @@ CONE_ZERO, CONE_NONNEG, CONE_SOC, CONE_EXP = range(4)
 RECIPE_DIRECT, RECIPE_NORMAL = 0, 1
 
 ST_K, ST_SINCE, ST_STATUS, ST_CGT, ST_PR, ST_DR, ST_GAP, ST_LASTCG = range(8)
+ST_TAU, ST_KAPPA, ST_DENOM, ST_EPOCH, ST_SETUP_CG = range(8, 13)
+MAX_RANKS = 8
+MBOX_STRIDE = 24
 STATE_LEN = 16
 
 _i32, _i64, _f64, _vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -82,6 +85,26 @@ class ScsWorkC(ctypes.Structure):
                                      "q", "t", "state")]
 
 
+class ShardCommC(ctypes.Structure):
+    _fields_ = [("world", _i32), ("rank", _i32), ("x_begin", _i64 * (MAX_RANKS + 1)),
+                ("inbox", _vp * MAX_RANKS), ("xfull", _vp * MAX_RANKS),
+                ("mbox", _vp * MAX_RANKS)]
+
+
+class ShardProblemC(ctypes.Structure):
+    _fields_ = [("struct_size", _i64), ("n", _i64), ("m", _i64), ("A", _vp), ("K", _vp),
+                ("b", _vp), ("c", _vp), ("pr_scale", _f64), ("dr_scale", _f64),
+                ("setup_tol", _f64)]
+
+    def __init__(self, **kw):
+        super().__init__(struct_size=ctypes.sizeof(ShardProblemC), **kw)
+
+
+class ShardWorkC(ctypes.Structure):
+    _fields_ = [(nm, _vp) for nm in ("cgx", "gx", "p", "wx", "gxs", "wy", "vy", "uy", "tax",
+                                     "t", "gy", "state")]
+
+
 # every symbol include/cgb200.h declares, with its ctypes signature
 SIGNATURES = {
     "cgb_abi_version": (ctypes.c_int, []),
@@ -106,6 +129,18 @@ SIGNATURES = {
                                        ctypes.POINTER(CgResult), ctypes.POINTER(_f64), _vp]),
     "cgb_debug_barrier": (ctypes.c_int, [_vp, _i64, ctypes.c_int, _vp]),
     "cgb_scs_profile": (ctypes.c_int, [_vp, _vp]),
+    "cgb_ctx_set_grid": (ctypes.c_int, [_vp, _i32]),
+    "cgb_shard_cones_create": (ctypes.c_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i64),
+                                              ctypes.POINTER(_i64), ctypes.POINTER(_i32),
+                                              ctypes.POINTER(_i32), _i32, _i64, _i32,
+                                              ctypes.POINTER(_vp)]),
+    "cgb_shard_run": (ctypes.c_int, [_vp, ctypes.POINTER(ShardProblemC),
+                                     ctypes.POINTER(ScsSettingsC), ctypes.POINTER(ShardCommC),
+                                     ctypes.POINTER(ShardWorkC), ctypes.c_int, _i64, _vp]),
+    "cgb_ipc_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
+    "cgb_ipc_open": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "cgb_ipc_close": (ctypes.c_int, [_vp]),
+    "cgb_ipc_free": (ctypes.c_int, [_vp]),
 }
 
 
@@ -147,12 +182,14 @@ def check(rc: int) -> None:
 class _Context:
     """Per-device persistent-kernel context (grid barrier + reduction banks)."""
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, grid: int = 0):
         lib = load_library()
         h = _vp()
         check(lib.cgb_ctx_create(device, ctypes.byref(h)))
         self.handle = h
         self.device = device
+        if grid:
+            check(lib.cgb_ctx_set_grid(h, int(grid)))
 
     def geometry(self):
         out = (_i32 * 3)()
@@ -161,6 +198,12 @@ class _Context:
 
 
 _ctxs: dict[int, _Context] = {}
+
+
+def new_context(device: int, grid: int = 0) -> _Context:
+    """A private cgb_ctx (own grid barrier and reduction banks), e.g. one per
+    rank when several ranks of a sharded solve share a device."""
+    return _Context(device, grid)
 
 
 def device_context():

@@ -393,8 +393,8 @@ def _leaf_flops(leaf: _lib.Leaf, nnz: int) -> int:
 class DeviceOp:
     """Compiled forward + adjoint plans of one expression (a cgb_op)."""
 
-    def __init__(self, expr):
-        self.ctx = _lib.device_context()
+    def __init__(self, expr, ctx=None):
+        self.ctx = ctx if ctx is not None else _lib.device_context()
         self.rows, self.cols = expr.rows, expr.cols
         self.fwd = _Builder()
         self.fwd.emit(expr, False, 0, 0, 0, 0, 1.0, 0)

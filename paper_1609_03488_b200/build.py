@@ -8,6 +8,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "cgb200.cu")
 DEPS = [SRC, os.path.join(HERE, "csrc", "cgb_device.cuh"),
+        os.path.join(HERE, "csrc", "cgb_shard.cuh"),
+        os.path.join(HERE, "csrc", "cgb_shard_kernel.cuh"),
         os.path.join(os.path.dirname(HERE), "include", "cgb200.h")]
 OUT = os.path.join(HERE, "lib", "libcgb200.so")
 
@@ -31,7 +33,7 @@ def up_to_date() -> bool:
 
 # translation units compiled in parallel (see the CGB_TU_* flags in cgb200.cu)
 UNITS = ["CGB_TU_HOST", "CGB_TU_SCS0", "CGB_TU_SCS1", "CGB_TU_CG", "CGB_TU_INNER",
-         "CGB_TU_MISC"]
+         "CGB_TU_MISC", "CGB_TU_SHARD"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

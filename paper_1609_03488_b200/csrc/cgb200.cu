@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "cgb_device.cuh"
+#include "cgb_shard.cuh"
 
 // Translation units: by default this file defines everything.  The build
 // (build.py) compiles it several times in parallel with -DCGB_SPLIT and one
@@ -38,6 +39,7 @@
 #define CGB_TU_CG 1
 #define CGB_TU_INNER 1
 #define CGB_TU_MISC 1
+#define CGB_TU_SHARD 1
 #endif
 #ifndef CGB_TU_HOST
 #define CGB_TU_HOST 0
@@ -56,6 +58,9 @@
 #endif
 #ifndef CGB_TU_MISC
 #define CGB_TU_MISC 0
+#endif
+#ifndef CGB_TU_SHARD
+#define CGB_TU_SHARD 0
 #endif
 
 using namespace cgb;
@@ -1190,6 +1195,8 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_co
 #endif
 
 
+#include "cgb_shard_kernel.cuh"
+
 // explicit instantiations, one group per translation unit
 #if CGB_TU_SCS0
 template __global__ void k_scs<false>(const __grid_constant__ ScsArgs);
@@ -1204,6 +1211,9 @@ template __global__ void k_cg<true>(const __grid_constant__ CgArgs);
 #if CGB_TU_INNER
 template __global__ void k_inner<false>(const __grid_constant__ InnerArgs);
 template __global__ void k_inner<true>(const __grid_constant__ InnerArgs);
+#endif
+#if CGB_TU_SHARD
+template __global__ void k_shard<false>(const __grid_constant__ ShardArgs);
 #endif
 #if CGB_TU_MISC
 template __global__ void k_apply<false>(const __grid_constant__ ApplyArgs);
@@ -1268,6 +1278,7 @@ struct cgb_op {
 
 struct cgb_cones {
   const cgb_ctx* ctx = nullptr;
+  bool sharded = false;      // pieces of a row-sharded problem (k_shard only)
   DevCones dc{};
   void* blob = nullptr;
   int64_t m = 0;
@@ -1808,6 +1819,7 @@ int cgb_cones_project(cgb_ctx* ctx, const cgb_cones* K, int dual, const double* 
                       void* stream) {
   if (!ctx || !K || !v || !out) return fail(CGB_EINVAL, "null argument");
   if (v == out) return fail(CGB_EINVAL, "cgb_cones_project: in-place projection not supported");
+  if (K->sharded) return fail(CGB_EINVAL, "sharded cone pieces cannot be projected alone");
   if (K->ctx != ctx) return fail(CGB_EINVAL, "cones belong to another ctx");
   std::lock_guard<std::mutex> lk(ctx->mu);
   ConeArgs a{ctx->bar, ctx->partials, K->dc, dual, v, out};
@@ -1898,6 +1910,7 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   const cgb_op* op = prob->A;
   if (op->ctx != ctx || prob->K->ctx != ctx)
     return fail(CGB_EINVAL, "operator / cones belong to another ctx");
+  if (prob->K->sharded) return fail(CGB_EINVAL, "sharded cone pieces need cgb_shard_run");
   if (op->fwd.in_len != prob->n || op->fwd.out_len != prob->m || prob->K->m != prob->m)
     return fail(CGB_EINVAL, "problem dimensions disagree with operator / cones");
   if (st->check_interval < 1 || st->eps <= 0) return fail(CGB_EINVAL, "bad settings");
@@ -1939,6 +1952,176 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   if (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
     return launch_coop(ctx, k_scs<true>, a, smem, (cudaStream_t)stream);
   return launch_coop(ctx, k_scs<false>, a, smem, (cudaStream_t)stream);
+}
+
+int cgb_ctx_set_grid(cgb_ctx* ctx, int32_t grid) {
+  if (!ctx || grid < 0) return fail(CGB_EINVAL, "bad argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->grid_override = grid;
+  return CGB_OK;
+}
+
+int cgb_shard_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* begin,
+                           const int64_t* end, const int32_t* soc_id, const int32_t* has_head,
+                           int32_t npieces, int64_t m, int32_t nsoc, cgb_cones** out) {
+  if (!ctx || !out || npieces < 0 || (npieces > 0 && (!kinds || !begin || !end || !soc_id ||
+                                                      !has_head)))
+    return fail(CGB_EINVAL, "bad cone piece spec");
+  if (nsoc < 0 || nsoc > CGB_MAX_LARGE_SOC)
+    return fail(CGB_EINVAL, "at most " + std::to_string(CGB_MAX_LARGE_SOC) +
+                                " world-reduced second-order cones");
+  *out = nullptr;
+  std::vector<DevSeg> segs;
+  std::vector<int64_t> small_off, exp_off;
+  std::vector<int32_t> small_dim;
+  int64_t prev = 0;
+  for (int i = 0; i < npieces; ++i) {
+    const int64_t b0 = begin[i], e0 = end[i];
+    if (b0 != prev || e0 <= b0 || e0 > m)
+      return fail(CGB_EINVAL, "cone pieces must tile [0, m) in order");
+    prev = e0;
+    switch (kinds[i]) {
+      case CGB_CONE_ZERO:
+      case CGB_CONE_NONNEG: {
+        const int32_t kind = kinds[i] == CGB_CONE_ZERO ? SEG_ZERO : SEG_NONNEG;
+        if (!segs.empty() && segs.back().kind == kind && segs.back().end == b0)
+          segs.back().end = e0;
+        else
+          segs.push_back(DevSeg{b0, e0, kind, 0});
+      } break;
+      case CGB_CONE_SOC:
+        if (soc_id[i] >= 0) {
+          if (soc_id[i] >= nsoc) return fail(CGB_EINVAL, "soc_id out of range");
+          segs.push_back(DevSeg{b0, e0, has_head[i] ? SEG_SOC_LARGE : SEG_SOC_TAIL, soc_id[i]});
+        } else {
+          if (e0 - b0 > INT32_MAX) return fail(CGB_EINVAL, "SOC too large");
+          small_off.push_back(b0);
+          small_dim.push_back((int32_t)(e0 - b0));
+        }
+        break;
+      case CGB_CONE_EXP:
+        if (e0 - b0 != 3) return fail(CGB_EINVAL, "exponential cone piece must be whole (3)");
+        exp_off.push_back(b0);
+        break;
+      default:
+        return fail(CGB_EINVAL, "unknown cone kind");
+    }
+  }
+  if (prev != m) return fail(CGB_EINVAL, "cone pieces must tile [0, m)");
+  Blob blob;
+  size_t o_seg = blob.add(segs.data(), sizeof(DevSeg) * segs.size());
+  size_t o_so = blob.add(small_off.data(), sizeof(int64_t) * small_off.size());
+  size_t o_sd = blob.add(small_dim.data(), sizeof(int32_t) * small_dim.size());
+  size_t o_eo = blob.add(exp_off.data(), sizeof(int64_t) * exp_off.size());
+  char* dev = nullptr;
+  CUDA_TRY(cudaMalloc(&dev, blob.host.size() + 256));
+  CUDA_TRY(cudaMemcpy(dev, blob.host.data(), blob.host.size(), cudaMemcpyHostToDevice));
+  cgb_cones* K = new cgb_cones();
+  K->ctx = ctx;
+  K->sharded = true;
+  K->blob = dev;
+  K->m = m;
+  K->segs = segs;
+  DevCones& C = K->dc;
+  C.seg = (const DevSeg*)(dev + o_seg);
+  C.small_off = (const int64_t*)(dev + o_so);
+  C.small_dim = (const int32_t*)(dev + o_sd);
+  C.exp_off = (const int64_t*)(dev + o_eo);
+  C.m = m;
+  C.nseg = (int32_t)segs.size();
+  C.nsmall = (int32_t)small_off.size();
+  C.nexp = (int32_t)exp_off.size();
+  C.nlarge = nsoc;
+  *out = K;
+  return CGB_OK;
+}
+
+int cgb_shard_run(cgb_ctx* ctx, const cgb_shard_problem* prob, const cgb_scs_settings* st,
+                  const cgb_shard_comm* comm, cgb_shard_work* work, int mode,
+                  int64_t max_steps, void* stream) {
+  if (!ctx || !prob || !st || !comm || !work) return fail(CGB_EINVAL, "null argument");
+  if (prob->struct_size != (int64_t)sizeof(cgb_shard_problem))
+    return fail(CGB_EINVAL, "cgb_shard_problem.struct_size mismatch");
+  if (!prob->A || !prob->K || !prob->b || !prob->c) return fail(CGB_EINVAL, "null problem member");
+  if (mode != 0 && mode != 1) return fail(CGB_EINVAL, "mode must be 0 (setup) or 1 (iterate)");
+  const int R = comm->world, me = comm->rank;
+  if (R < 1 || R > CGB_MAX_RANKS || me < 0 || me >= R)
+    return fail(CGB_EINVAL, "world size must be 1.." + std::to_string(CGB_MAX_RANKS));
+  if (comm->x_begin[0] != 0 || comm->x_begin[R] != prob->n)
+    return fail(CGB_EINVAL, "x slices must tile [0, n)");
+  for (int q = 0; q < R; ++q) {
+    if (comm->x_begin[q + 1] < comm->x_begin[q]) return fail(CGB_EINVAL, "x slices out of order");
+    if (!comm->inbox[q] || !comm->xfull[q] || !comm->mbox[q])
+      return fail(CGB_EINVAL, "null peer buffer of rank " + std::to_string(q));
+  }
+  const cgb_op* op = prob->A;
+  if (op->ctx != ctx || prob->K->ctx != ctx)
+    return fail(CGB_EINVAL, "operator / cones belong to another ctx");
+  if (op->fwd.in_len != prob->n || op->fwd.out_len != prob->m || prob->K->m != prob->m)
+    return fail(CGB_EINVAL, "problem dimensions disagree with operator / cones");
+  if (op->fwd.dp.smem_xs2 > 0 || op->adj.dp.smem_xs2 > 0)
+    return fail(CGB_EINVAL, "2-d convolution leaves are not row-sharded (keep them on one GPU)");
+  if (st->check_interval < 1 || st->eps <= 0) return fail(CGB_EINVAL, "bad settings");
+  if (max_steps < 0) return CGB_OK;  // validation only (launch nothing)
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ShardArgs a;
+  a.bar = ctx->bar;
+  a.partials = ctx->partials;
+  a.F = op->fwd.dp;
+  a.Aj = op->adj.dp;
+  a.K = prob->K->dc;
+  a.st = *st;
+  a.comm = *comm;
+  a.w = *work;
+  a.b = prob->b;
+  a.c = prob->c;
+  a.n = prob->n;
+  a.m = prob->m;
+  a.x0 = comm->x_begin[me];
+  a.nl = comm->x_begin[me + 1] - comm->x_begin[me];
+  a.pr_scale = prob->pr_scale;
+  a.dr_scale = prob->dr_scale;
+  a.eps_floor = eps_floor_for(prob->n);
+  a.setup_tol = prob->setup_tol;
+  a.max_steps = max_steps;
+  a.mode = mode;
+  return launch_coop(ctx, k_shard<false>, a, solver_smem(a.F, a.Aj), (cudaStream_t)stream);
+}
+
+int cgb_ipc_alloc(int device, int64_t bytes, void** ptr, void* handle64) {
+  if (!ptr || !handle64 || bytes < 0) return fail(CGB_EINVAL, "bad argument");
+  CUDA_TRY(cudaSetDevice(device));
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, (size_t)std::max<int64_t>(bytes, 256)));
+  CUDA_TRY(cudaMemset(p, 0, (size_t)std::max<int64_t>(bytes, 256)));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(CGB_ECUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  std::memcpy(handle64, &h, sizeof(h));
+  *ptr = p;
+  return CGB_OK;
+}
+
+int cgb_ipc_open(int device, const void* handle64, void** ptr) {
+  if (!ptr || !handle64) return fail(CGB_EINVAL, "bad argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return CGB_OK;
+}
+
+int cgb_ipc_close(void* ptr) {
+  if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return CGB_OK;
+}
+
+int cgb_ipc_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFree(ptr));
+  return CGB_OK;
 }
 
 int cgb_scs_profile(cgb_ctx* ctx, double* dev_acc) {

@@ -96,7 +96,7 @@ struct DevPlan {
   int64_t in_len, out_len;
 };
 
-enum SegKind : int32_t { SEG_ZERO = 0, SEG_NONNEG = 1, SEG_SOC_LARGE = 2 };
+enum SegKind : int32_t { SEG_ZERO = 0, SEG_NONNEG = 1, SEG_SOC_LARGE = 2, SEG_SOC_TAIL = 3 };
 
 struct DevSeg {
   int64_t begin, end;
