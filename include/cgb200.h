@@ -52,6 +52,10 @@ extern "C" {
 #define CGB_LEAF_CORR1D 4   /* valid corr (adjoint of CONV1D): rows n0, cols n0+k0-1 */
 #define CGB_LEAF_CONV2D 5   /* full 2-d conv of n0 x n1 image, kernel k0 x k1 */
 #define CGB_LEAF_CORR2D 6   /* valid 2-d corr (adjoint of CONV2D)             */
+/* cgb_leaf.reserved flag for CONV2D / CORR2D: the kernel is rank one
+ * (K = u v^T), apply it as a column pass and a row pass.  The library
+ * re-verifies the factorization and applies K directly if it fails.       */
+#define CGB_LEAF_FLAG_SEPARABLE 1
 
 typedef struct cgb_leaf {
   int32_t kind;

@@ -22,6 +22,7 @@ CGB_EINVAL = -1
 CGB_ENODEV = -2
 
 LEAF_IDENTITY, LEAF_DENSE, LEAF_CSR, LEAF_CONV1D, LEAF_CORR1D, LEAF_CONV2D, LEAF_CORR2D = range(7)
+LEAF_FLAG_SEPARABLE = 1
 CONE_ZERO, CONE_NONNEG, CONE_SOC, CONE_EXP = range(4)
 RECIPE_DIRECT, RECIPE_NORMAL = 0, 1
 

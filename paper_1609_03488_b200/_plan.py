@@ -37,6 +37,24 @@ def _scaled_identity(e) -> float | None:
     return None
 
 
+SEPARABLE_KMAX = 63   # CGB_SEP_KMAX
+
+
+def separable(kernel: np.ndarray) -> bool:
+    """A 2-d kernel of numerical rank one (sigma_2 <= 1e-13 sigma_1) is
+    applied as a column pass and a row pass (kh + kw instead of kh * kw
+    multiply-adds per output; the library re-verifies the factorization
+    entrywise).  CGB_NO_SEPARABLE=1 forces the direct 2-d sum."""
+    import os
+    if os.environ.get("CGB_NO_SEPARABLE"):
+        return False
+    k = np.asarray(kernel, dtype=np.float64)
+    if k.ndim != 2 or k.shape[1] > SEPARABLE_KMAX or not np.any(k):
+        return False
+    s = np.linalg.svd(k, compute_uv=False)
+    return len(s) < 2 or s[1] <= 1e-13 * s[0]
+
+
 def _cuda(a: np.ndarray, dtype=None):
     import torch
     t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else a.astype(dtype)))
@@ -189,7 +207,9 @@ class _Builder:
                 kind = _lib.LEAF_CORR2D if adj else _lib.LEAF_CONV2D
                 rows, cols = (e.cols, e.rows) if adj else (e.rows, e.cols)
                 return _lib.Leaf(kind=kind, rows=rows, cols=cols, val=t.data_ptr(), k0=kh,
-                                 k1=kw, n0=h, n1=w), 0
+                                 k1=kw, n0=h, n1=w,
+                                 reserved=_lib.LEAF_FLAG_SEPARABLE if separable(e.kernel)
+                                 else 0), 0
             return self._add_leaf((id(e), adj), make)
         raise L.LinOpError(f"no device leaf for {type(e).__name__}")
 
@@ -386,6 +406,8 @@ def _leaf_flops(leaf: _lib.Leaf, nnz: int) -> int:
     if k in (_lib.LEAF_CONV1D, _lib.LEAF_CORR1D):
         return 2 * leaf.n0 * leaf.k0          # every signal sample meets every tap once
     if k in (_lib.LEAF_CONV2D, _lib.LEAF_CORR2D):
+        if leaf.reserved & _lib.LEAF_FLAG_SEPARABLE:   # column pass + row pass per output
+            return 2 * leaf.rows * (leaf.k0 + leaf.k1)
         return 2 * leaf.n0 * leaf.n1 * leaf.k0 * leaf.k1
     return 0
 

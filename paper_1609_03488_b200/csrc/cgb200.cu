@@ -1287,7 +1287,7 @@ struct cgb_cones {
 
 namespace {
 
-size_t plan_smem(const DevPlan& P) { return sizeof(double) * CGB_WARPS * (size_t)P.smem_per_warp; }
+size_t plan_smem(const DevPlan& P) { return sizeof(double) * (size_t)P.smem_total; }
 
 // dynamic shared memory of a solver kernel: the plans' conv staging
 size_t solver_smem(const DevPlan& F, const DevPlan& Aj) {
@@ -1303,7 +1303,7 @@ int grid_for(const cgb_ctx* ctx, K kernel, size_t smem, int* grid) {
   if (per_sm < 1)
     return fail(CGB_ECOOP, "kernel cannot be resident (threads/registers/shared memory)");
   // one CTA per SM: the persistent kernels size every loop to the grid
-  int g = std::min(ctx->num_sms, CGB_MAXG);
+  int g = std::min(ctx->num_sms * std::min(per_sm, CGB_CTAS_PER_SM), CGB_MAXG);
   if (ctx->grid_override > 0) g = std::min(g, ctx->grid_override);
   *grid = g;
   return CGB_OK;
@@ -1525,7 +1525,7 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       for (int t = R.term_begin; t < R.term_end; ++t)
         has_dense |= d->leaves[d->terms[t].leaf].kind == CGB_LEAF_DENSE;
       D.rpt = 32 * D.rfac;
-      D.pad = 0;
+      D.strip_term = -1;
       if (period > 0 && periodic_ok) {
         D.rfac = CGB_RC;
         D.rpt = 32 * CGB_RC;
@@ -1547,8 +1547,42 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   // correlation taps of the tiled 1-d conv leaves (reversed for conv)
   std::vector<int32_t> leaf_taps(std::max(1, d->nleaves), -1);
   std::vector<double> taps;
+  std::vector<cgb_leaf> leaves(d->leaves, d->leaves + d->nleaves);
   for (int i = 0; i < d->nleaves; ++i) {
-    const cgb_leaf& L = d->leaves[i];
+    cgb_leaf& L = leaves[i];
+    const bool is2d = L.kind == CGB_LEAF_CONV2D || L.kind == CGB_LEAF_CORR2D;
+    if (!is2d) L.reserved = 0;
+    if (is2d && (L.reserved & CGB_LEAF_FLAG_SEPARABLE) && L.k1 <= CGB_SEP_KMAX &&
+        L.k0 + (L.k1 + CGB_RC - 1) / CGB_RC * CGB_RC <= 4096) {
+      // rank-one factorization through the largest entry (a*, b*):
+      // u[a] = K[a, b*], v[b] = K[a*, b] / K[a*, b*]; kept only if it
+      // reproduces every entry to a few ulp of max |K|
+      std::vector<double> kv(L.k0 * L.k1);
+      CUDA_TRY(cudaMemcpy(kv.data(), L.val, sizeof(double) * kv.size(), cudaMemcpyDeviceToHost));
+      int64_t pa = 0, pb = 0;
+      double pmax = 0.0;
+      for (int64_t a = 0; a < L.k0; ++a)
+        for (int64_t b = 0; b < L.k1; ++b)
+          if (std::fabs(kv[a * L.k1 + b]) > pmax) { pmax = std::fabs(kv[a * L.k1 + b]); pa = a; pb = b; }
+      std::vector<double> u(L.k0), v(L.k1);
+      bool ok = pmax > 0.0;
+      if (ok) {
+        for (int64_t a = 0; a < L.k0; ++a) u[a] = kv[a * L.k1 + pb];
+        for (int64_t b = 0; b < L.k1; ++b) v[b] = kv[pa * L.k1 + b] / kv[pa * L.k1 + pb];
+        for (int64_t a = 0; a < L.k0 && ok; ++a)
+          for (int64_t b = 0; b < L.k1 && ok; ++b)
+            ok = std::fabs(kv[a * L.k1 + b] - u[a] * v[b]) <= 8.0 * DBL_EPSILON * pmax;
+      }
+      if (ok) {
+        const int64_t nt = (L.k1 + CGB_RC - 1) / CGB_RC * CGB_RC;
+        leaf_taps[i] = (int32_t)taps.size();
+        for (int64_t j = 0; j < nt; ++j)
+          taps.push_back(j < L.k1 ? v[L.kind == CGB_LEAF_CONV2D ? L.k1 - 1 - j : j] : 0.0);
+        for (int64_t a = 0; a < L.k0; ++a) taps.push_back(u[a]);
+        continue;
+      }
+    }
+    L.reserved = 0;
     if ((L.kind == CGB_LEAF_CONV1D || L.kind == CGB_LEAF_CORR1D) && L.k0 <= CGB_CONV_KMAX) {
       std::vector<double> kv(L.k0);
       CUDA_TRY(cudaMemcpy(kv.data(), L.val, sizeof(double) * L.k0, cudaMemcpyDeviceToHost));
@@ -1570,8 +1604,56 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
                                   : 0.0);
     }
   }
+  // 2-d conv row blocks as CTA strips (run_strips): a periodic block whose
+  // only 2-d term has device taps and whose other terms are identity /
+  // sparse / dense; the CTA ring of kh + 15 input-row slots overlays the
+  // per-warp buffers.  CGB_STRIP=0 disables (A/B), CGB_STRIP_ROWS sets the
+  // output rows per task.
+  int32_t strip_slot = 0, strip_nslot = 0, strip_rows = 0;
+  {
+    const char* env = std::getenv("CGB_STRIP");
+    const bool allow = !(env && env[0] == '0');
+    int64_t khmax = 0, ntmax = 0;
+    for (size_t i = 0; i < rbs.size() && allow; ++i) {
+      DevRowBlock& D = rbs[i];
+      if (D.period <= 0) continue;
+      int n2 = 0, t2 = -1;
+      bool others_ok = true;
+      for (int t = D.term_begin; t < D.term_end; ++t) {
+        const cgb_leaf& LF = leaves[d->terms[t].leaf];
+        if (LF.kind == CGB_LEAF_CONV2D || LF.kind == CGB_LEAF_CORR2D) {
+          ++n2;
+          t2 = t;
+        } else if (LF.kind != CGB_LEAF_IDENTITY && LF.kind != CGB_LEAF_CSR &&
+                   LF.kind != CGB_LEAF_DENSE) {
+          others_ok = false;
+        }
+      }
+      if (n2 != 1 || !others_ok || leaf_taps[d->terms[t2].leaf] < 0) continue;
+      const cgb_leaf& LF = leaves[d->terms[t2].leaf];
+      const int64_t nt = (LF.k1 + CGB_RC - 1) / CGB_RC * CGB_RC;
+      const int64_t slot = (32 * CGB_RC + nt + 2 + 1) & ~1;
+      const int64_t need = (LF.k0 + 15) * slot + CGB_WARPS * (slot + 32 * CGB_RC + 2);
+      if (need > 24 * 1024) continue;  // 192 KB of shared memory at most
+      D.strip_term = t2;
+      khmax = std::max<int64_t>(khmax, LF.k0);
+      ntmax = std::max<int64_t>(ntmax, nt);
+    }
+    const int64_t slot_all = (32 * CGB_RC + ntmax + 2 + 1) & ~1;
+    if (khmax > 0 && (khmax + 15) * slot_all + CGB_WARPS * (slot_all + 32 * CGB_RC + 2) > 24 * 1024) {
+      for (DevRowBlock& D : rbs) D.strip_term = -1;   // several kernels: over budget together
+      khmax = 0;
+    }
+    if (khmax > 0) {
+      strip_slot = (int32_t)((32 * CGB_RC + ntmax + 2 + 1) & ~1);
+      strip_nslot = (int32_t)(khmax + 15);
+      int rows = 32;
+      if (const char* er = std::getenv("CGB_STRIP_ROWS")) rows = std::max(8, std::atoi(er) / 8 * 8);
+      strip_rows = rows;
+    }
+  }
   Blob blob;
-  size_t o_leaves = blob.add(d->leaves, sizeof(cgb_leaf) * d->nleaves);
+  size_t o_leaves = blob.add(leaves.data(), sizeof(cgb_leaf) * d->nleaves);
   size_t o_terms = blob.add(d->terms, sizeof(cgb_term) * d->nterms);
   size_t o_rbs = blob.add(rbs.data(), sizeof(DevRowBlock) * rbs.size());
   size_t o_lrb = blob.add(level_rb.data(), sizeof(int32_t) * level_rb.size());
@@ -1617,6 +1699,13 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   }
   if (kmax > 0 || kw2max > 0)
     P.smem_per_warp = 2 * P.smem_xs + (32 * CGB_RC + 2) + CGB_RING2 * P.smem_xs2;
+  P.strip_slot = strip_slot;
+  P.strip_nslot = strip_nslot;
+  P.strip_rows = strip_rows;
+  P.smem_total = CGB_WARPS * P.smem_per_warp;
+  if (P.strip_rows > 0)
+    P.smem_total = std::max<int32_t>(
+        P.smem_total, P.strip_nslot * P.strip_slot + CGB_WARPS * (P.strip_slot + 32 * CGB_RC + 2));
   P.in_len = d->in_len;
   P.out_len = d->out_len;
   ps->in_len = d->in_len;
@@ -1940,7 +2029,7 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   // cone step, whichever is larger (never live together; one CTA per SM --
   // the kernel re-checks the stash need with the real grid)
   const size_t base = solver_smem(a.F, a.Aj);
-  const int64_t S = (int64_t)std::min(ctx->num_sms, CGB_MAXG) * CGB_BLOCK;
+  const int64_t S = (int64_t)std::min(ctx->num_sms * CGB_CTAS_PER_SM, CGB_MAXG) * CGB_BLOCK;
   int64_t need = 0;
   for (const DevSeg& sg : prob->K->segs)
     if (sg.kind == SEG_SOC_LARGE)

@@ -20,7 +20,12 @@
 #ifndef CGB_BAR_FENCE
 #define CGB_BAR_FENCE 1      // grid-barrier fence flavour (see GridSync::sync)
 #endif
-#define CGB_MAXG 160         // largest grid the reductions are unrolled for (148 SMs x 1)
+#ifndef CGB_CTAS_PER_SM
+#define CGB_CTAS_PER_SM CGB_MINB  // persistent CTAs per SM (grid = SMs x this)
+#endif
+#ifndef CGB_MAXG
+#define CGB_MAXG (160 * CGB_CTAS_PER_SM)  // largest grid the reductions are unrolled for
+#endif
 #define CGB_MAX_LARGE_SOC 4  // SOC blocks reduced across the whole grid
 #ifndef CGB_RC
 #define CGB_RC 9             // rows per lane in convolution tiles (odd: no bank conflicts)
@@ -32,6 +37,7 @@
 #define CGB_DENSE_UNROLL 4   // dense GEMV: column chunks unrolled per row group
 #endif
 #define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
+#define CGB_SEP_KMAX 63      // widest rank-one 2-d kernel applied as column + row passes
 #ifndef CGB_U
 #define CGB_U 8              // elements per thread per batch in streaming loops
 #endif
@@ -50,7 +56,7 @@ struct DevRowBlock {
   int32_t conv_term;  // the block's only 1-d conv term (TMA-staged), or -1
   int32_t tpr;        // periodic blocks: tiles per row
   int32_t rpt;        // rows per tile (32 * rfac, or fewer for dense blocks)
-  int32_t pad;
+  int32_t strip_term; // periodic blocks: the 2-d conv term run as CTA strips, or -1
 };
 
 // first row and row count of a tile of row block rb
@@ -93,6 +99,10 @@ struct DevPlan {
   int32_t smem_xs;        // one staged-input window; two windows, then the
                           // 32*RC+1 output transpose, then the 2-d ring
   int32_t smem_xs2;       // one 2-d conv row window (CGB_RING2 of them)
+  int32_t strip_slot;     // 2-d strips: doubles per input-row slot of the CTA ring
+  int32_t strip_nslot;    // slots in the ring (kh + 15)
+  int32_t strip_rows;     // output rows per strip task (multiple of CGB_WARPS)
+  int32_t smem_total;     // doubles of dynamic shared memory the plan needs per CTA
   int64_t in_len, out_len;
 };
 
@@ -198,6 +208,10 @@ __device__ __forceinline__ void issue_bulk(double* dst, const double* src, uint3
 #define CGB_RING2 4  // row windows in flight per warp in a 2-d conv tile
 __shared__ uint64_t cgb_mbar[CGB_WARPS][2 + CGB_RING2];
 __shared__ uint32_t cgb_mbar_phase[CGB_WARPS];
+// CTA-level mbarriers of the 2-d strip row ring (batch g uses g & 1) and the
+// number of batches this CTA has issued
+__shared__ uint64_t cgb_strip_mbar[2];
+__shared__ uint32_t cgb_strip_seq;
 
 // every persistent kernel calls this first (all threads)
 __device__ __forceinline__ void tma_init() {
@@ -207,7 +221,13 @@ __device__ __forceinline__ void tma_init() {
     cgb_mbar_phase[wib] = 0;
     fence_mbar_init();
   }
-  if (threadIdx.x == 0) cgb_tl_acc = nullptr;
+  if (threadIdx.x == 0) {
+    cgb_tl_acc = nullptr;
+    mbar_init(&cgb_strip_mbar[0], 1);
+    mbar_init(&cgb_strip_mbar[1], 1);
+    cgb_strip_seq = 0;
+    fence_mbar_init();
+  }
   __syncthreads();
 }
 
@@ -582,6 +602,16 @@ static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0
   }
   const int nrows = (int)(a_hi - a_lo + 1);
   const bool tma = clo >= 0 && clo + span <= IW;
+  // rank-one kernel K = u v^T (CGB_LEAF_FLAG_SEPARABLE): each row window is
+  // folded into column sums t = sum_a u[a] x_a (a lane per 32-strided window
+  // position), then ONE row correlation y = v * t -- kh + kw multiply-adds
+  // per output instead of kh * kw.  taps = [v row taps | u (kh)].
+  const bool sep = (L.reserved & CGB_LEAF_FLAG_SEPARABLE) != 0;
+  constexpr int kSepQ = (32 * CGB_RC + CGB_SEP_KMAX + 31) / 32;
+  double tcol[kSepQ];
+#pragma unroll
+  for (int q = 0; q < kSepQ; ++q) tcol[q] = 0.0;
+  const int nq = (span + 31) / 32;
   auto issue = [&](int idx) {
     const int64_t a = a_lo + idx;
     const int64_t xi = conv ? oi - a : oi + a;
@@ -611,11 +641,32 @@ static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0
       stage_row(rowp, clo, IW, span, xs, lane);
     }
     __syncwarp();
-    conv_accum(kw, xs + sh, taps + a * ntaps, y, lane);
+    if (sep) {
+      const double ua = taps[ntaps + a];
+#pragma unroll
+      for (int q = 0; q < kSepQ; ++q) {
+        const int ix = lane + 32 * q;
+        if (q < nq && ix < span) tcol[q] = fma(ua, xs[sh + ix], tcol[q]);
+      }
+    } else {
+      conv_accum(kw, xs + sh, taps + a * ntaps, y, lane);
+    }
     if (tma && i + CGB_RING2 < nrows) issue(i + CGB_RING2);
   }
   if (lane == 0) cgb_mbar_phase[wib] = (cgb_mbar_phase[wib] & 3u) | (ph << 2);
   __syncwarp();
+  if (sep) {
+    // every ring copy of this tile has been waited for: slot 0 holds t
+    double* ts = ring;
+#pragma unroll
+    for (int q = 0; q < kSepQ; ++q) {
+      const int ix = lane + 32 * q;
+      if (q < nq && ix < span) ts[ix] = tcol[q];
+    }
+    __syncwarp();
+    conv_accum(kw, ts, taps, y, lane);
+    __syncwarp();
+  }
   tile_transpose(y, os, acc, alpha, nvalid, lane);
 }
 
@@ -631,8 +682,7 @@ template <bool WITH2D>
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
                                           double (&acc)[CGB_RC], int lane, const double* cc,
-                                          double* xs, double* os, double* ring = nullptr,
-                                          int xs2 = 0) {
+                                          double* xs, double* os, double* ring, int xs2) {
   switch (L.kind) {
     case CGB_LEAF_IDENTITY: {
       double v[CGB_RC];
@@ -855,6 +905,308 @@ __device__ __forceinline__ void issue_window(const ConvWin& w, double* dst, uint
   }
 }
 
+// bulk copy only (the caller has announced the bytes on the mbarrier)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .b64 st;\n"
+      " mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+template <bool WITH2D>
+__device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
+                                          const InVec& in, double alpha,
+                                          double (&acc)[CGB_RC], int lane, const double* cc,
+                                          double* xs, double* os, double* ring, int xs2);
+
+// One output row segment of a strip: y = the conv of kernel rows
+// [a_lo, a_hi] with the ring's input rows (slot = input row mod NS); xrow0
+// != null: the rows came by TMA from x + row * IW (+ the copy's alignment
+// shift), else they were staged at the slot start.  Out of line: it holds
+// the column sums of the separable path in registers.
+static __device__ __noinline__ void strip_row(const cgb_leaf& L, int64_t oi, int64_t a_lo,
+                                              int64_t a_hi, const double* xrow0, int64_t IW,
+                                              const double* ring, int SLOT, int NS,
+                                              const double* taps, double* tb,
+                                              double (&yout)[CGB_RC], int lane) {
+  const bool conv = L.kind == CGB_LEAF_CONV2D;
+  const bool sep = (L.reserved & CGB_LEAF_FLAG_SEPARABLE) != 0;
+  const int64_t kw = L.k1;
+  const int ntaps = conv_ntaps(kw);
+  const int span = 32 * CGB_RC + ntaps;
+  double y[CGB_RC];  // registers (yout, by reference across the call, lives in memory)
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) y[r] = 0.0;
+  constexpr int kQ = (32 * CGB_RC + CGB_SEP_KMAX + 31) / 32;
+  double tcol[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) tcol[q] = 0.0;
+  const int nq = (span + 31) / 32;
+  for (int64_t a = a_lo; a <= a_hi; ++a) {
+    const int64_t xi = conv ? oi - a : oi + a;
+    const int sh = xrow0 ? (int)((reinterpret_cast<uintptr_t>(xrow0 + xi * IW) >> 3) & 1) : 0;
+    const double* xs = ring + (size_t)(xi % NS) * SLOT + sh;
+    if (sep) {
+      const double ua = taps[ntaps + a];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int ix = lane + 32 * q;
+        if (q < nq && ix < span) tcol[q] = fma(ua, xs[ix], tcol[q]);
+      }
+    } else {
+      conv_accum(kw, xs, taps + a * ntaps, y, lane);
+    }
+  }
+  if (sep) {
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int ix = lane + 32 * q;
+      if (q < nq && ix < span) tb[ix] = tcol[q];
+    }
+    __syncwarp();
+    conv_accum(kw, tb, taps, y, lane);
+  }
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) yout[r] = y[r];
+}
+
+// Separable strips, column pass of one step: t_j[c] = sum_a w[a] X(base0 + j + a)
+// for the CTA's CGB_WARPS output rows j, every thread a window column c,
+// with a sliding register window over the rows (one shared load per kh
+// multiply-adds per column and output row, conv_accum's scheme turned
+// vertical).  X(i) = input row base0 + i of the ring (zero outside
+// [0, IH)); w = u (corr) or u reversed (full conv); t_j goes to warp j's
+// buffer tbase + j * tstride.
+static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t base0, int64_t IH,
+                                                  int span, const double* ring, int SLOT, int NS,
+                                                  int sh0, int shodd, const double* u,
+                                                  double* tbase, int tstride) {
+  const bool conv = L.kind == CGB_LEAF_CONV2D;
+  const int kh = (int)L.k0;
+  const int s0 = (int)(((base0 % NS) + NS) % NS);
+  auto X = [&](int i, int c) -> double {
+    const int64_t r = base0 + i;
+    const int slot = s0 + i >= NS ? s0 + i - NS : s0 + i;
+    const int sh = (sh0 + (shodd & (int)(r & 1))) & 1;
+    const double v = ring[(size_t)slot * SLOT + sh + c];
+    return (r >= 0 && r < IH) ? v : 0.0;
+  };
+  for (int c = threadIdx.x; c < span; c += blockDim.x) {
+    double acc[CGB_WARPS], xw[CGB_WARPS];
+#pragma unroll
+    for (int j = 0; j < CGB_WARPS; ++j) {
+      acc[j] = 0.0;
+      xw[j] = X(j, c);
+    }
+    for (int g = 0; g < (kh + CGB_WARPS - 1) / CGB_WARPS; ++g) {
+#pragma unroll
+      for (int jj = 0; jj < CGB_WARPS; ++jj) {
+        const int a = CGB_WARPS * g + jj;
+        if (a < kh) {
+          const double wa = u[conv ? kh - 1 - a : a];
+#pragma unroll
+          for (int j = 0; j < CGB_WARPS; ++j)
+            acc[j] = fma(wa, xw[(jj + j) % CGB_WARPS], acc[j]);
+          if (a + 1 < kh) xw[jj] = X(a + CGB_WARPS, c);  // slot jj: row a -> row a + 8
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CGB_WARPS; ++j) tbase[(size_t)j * tstride + c] = acc[j];
+  }
+}
+
+// the row pass of a separable strip row: y = v * t (register-blocked)
+static __device__ __noinline__ void strip_rowpass(int64_t kw, const double* t, const double* taps,
+                                                  double (&yout)[CGB_RC], int lane) {
+  double y[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) y[r] = 0.0;
+  conv_accum(kw, t, taps, y, lane);
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) yout[r] = y[r];
+}
+
+// 2-d convolution row blocks as CTA strips.  A task is one 288-column
+// segment of a run of P.strip_rows consecutive output rows; the CTA's 8
+// warps compute 8 output rows per step (warp w: row 8 s + w) from a ring of
+// input rows in shared memory that every warp reads, so each input row of
+// the segment is brought in ONCE per task (the per-warp tile path re-reads
+// it kh times).  Rows arrive by TMA bulk copies in batches, one batch per
+// step, issued two steps ahead by thread 0 onto the two CTA mbarriers;
+// segments reaching past the image edge are staged by hand with zero fill.
+// Every other term of the block (identity, sparse, dense) and the epilogue
+// run per warp on its output row segment, exactly as in run_level.
+// Returns false (nothing done) when the apply input is a fused two-vector
+// accessor, which the strips do not stage.
+template <bool WITH2D, class Epi>
+__device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
+                           double* part) {
+  extern __shared__ __align__(16) double cgb_dyn_smem[];
+  if (!WITH2D || P.strip_rows == 0) return false;
+  if (in.b) return false;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int rb_lo = P.level_rb[e], rb_hi = P.level_rb[e + 1];
+  const double* temp = P.temp[ts];
+  const int SLOT = P.strip_slot, NS = P.strip_nslot;
+  double* ring = cgb_dyn_smem;
+  double* os = ring + (size_t)NS * SLOT + (size_t)wib * (SLOT + 32 * CGB_RC + 2);
+  double* tb = os + 32 * CGB_RC + 2;
+  bool any = false;
+  for (int rbi = rb_lo; rbi < rb_hi; ++rbi) {
+    const DevRowBlock rb = P.rbs[rbi];
+    if (rb.strip_term < 0) continue;
+    any = true;
+    const cgb_term tm = P.terms[rb.strip_term];
+    const cgb_leaf L = P.leaves[tm.leaf];
+    const bool conv = L.kind == CGB_LEAF_CONV2D;
+    const bool sep = (L.reserved & CGB_LEAF_FLAG_SEPARABLE) != 0;
+    const int64_t kh = L.k0, kw = L.k1;
+    const int64_t OW = conv ? L.n1 + kw - 1 : L.n1;
+    const int64_t IW = conv ? L.n1 : L.n1 + kw - 1;
+    const int64_t IH = conv ? L.n0 : L.n0 + kh - 1;
+    const int ntaps = conv_ntaps(kw);
+    const int span = 32 * CGB_RC + ntaps;
+    const double* taps = P.taps + P.leaf_taps[tm.leaf];
+    const double* x = tm.in_buf == 0 ? in.a + tm.in_off
+                                     : temp + P.temp_off[tm.in_buf - 1] + tm.in_off;
+    const int64_t oi_first = (rb.row_begin - tm.row_origin) / OW;
+    const int64_t prows = (rb.row_end - rb.row_begin) / OW;
+    const int64_t chunk = P.strip_rows;
+    const int64_t ntask = (prows + chunk - 1) / chunk * rb.tpr;
+    for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+      const int64_t ch = task / rb.tpr, pc = task - ch * rb.tpr;
+      const int64_t p0 = ch * chunk, p1 = p0 + chunk < prows ? p0 + chunk : prows;
+      const int64_t oj0 = pc * (32 * CGB_RC);
+      const int nvalid = (int)(OW - oj0 < 32 * CGB_RC ? OW - oj0 : 32 * CGB_RC);
+      const int64_t clo = conv ? oj0 - (kw - 1) : oj0;
+      const bool tma = clo >= 0 && clo + span <= IW;
+      const int nsteps = (int)((p1 - p0 + CGB_WARPS - 1) / CGB_WARPS);
+      // input rows first needed at step s, clipped to the image and to the
+      // rows this task's outputs reach
+      const int64_t row_hi = oi_first + p1 - 1 + (conv ? 0 : kh - 1) + 1;
+      auto batch = [&](int st, int64_t& r0, int64_t& r1) {
+        const int64_t lo = oi_first + p0 + (int64_t)CGB_WARPS * st - (conv ? kh - 1 : 0);
+        r0 = st == 0 ? lo : lo + kh - 1;
+        r1 = lo + kh - 1 + CGB_WARPS;
+        if (r0 < 0) r0 = 0;
+        if (r1 > IH) r1 = IH;
+        if (r1 > row_hi) r1 = row_hi;
+      };
+      auto row_src = [&](int64_t r, int& sh) {
+        const double* a = x + r * IW + clo;
+        sh = (int)((reinterpret_cast<uintptr_t>(a) >> 3) & 1);
+        return a - sh;
+      };
+      __syncthreads();                 // the previous task's rows are consumed
+      const uint32_t base = cgb_strip_seq;
+      __syncthreads();
+      auto issue = [&](int st) {       // thread 0: batch st onto mbarrier (base + st) & 1
+        int64_t r0, r1;
+        batch(st, r0, r1);
+        uint32_t total = 0;
+        for (int64_t r = r0; r < r1; ++r) {
+          int sh;
+          row_src(r, sh);
+          total += (uint32_t)(((span + sh) * 8 + 15) & ~15);
+        }
+        uint64_t* bar = &cgb_strip_mbar[(base + st) & 1u];
+        fence_proxy_async();
+        mbar_arrive_tx(bar, total);
+        for (int64_t r = r0; r < r1; ++r) {
+          int sh;
+          const double* src = row_src(r, sh);
+          bulk_copy(ring + (size_t)(r % NS) * SLOT, src, (uint32_t)(((span + sh) * 8 + 15) & ~15),
+                    bar);
+        }
+        cgb_strip_seq = base + st + 1;
+      };
+      if (tma && threadIdx.x == 0) {
+        issue(0);
+        if (nsteps > 1) issue(1);
+      }
+      for (int st = 0; st < nsteps; ++st) {
+        if (tma) {
+          const uint32_t g = base + st;
+          mbar_wait(&cgb_strip_mbar[g & 1u], (g >> 1) & 1u);
+        } else {
+          int64_t r0, r1;
+          batch(st, r0, r1);
+          for (int64_t r = r0 + wib; r < r1; r += CGB_WARPS)
+            stage_row(x + r * IW, clo, IW, span, ring + (size_t)(r % NS) * SLOT, lane);
+          __syncthreads();
+        }
+        const int64_t p = p0 + (int64_t)CGB_WARPS * st + wib;
+        if (sep) {
+          // all threads: column sums of the step's 8 output rows
+          const int64_t o0 = oi_first + p0 + (int64_t)CGB_WARPS * st;
+          const int sh0 = tma ? (int)((reinterpret_cast<uintptr_t>(x + clo) >> 3) & 1) : 0;
+          strip_colpass(L, conv ? o0 - (kh - 1) : o0, IH, span, ring, SLOT, NS, sh0,
+                        tma ? (int)(IW & 1) : 0, taps + ntaps,
+                        ring + (size_t)NS * SLOT + 32 * CGB_RC + 2, SLOT + 32 * CGB_RC + 2);
+          __syncthreads();
+        }
+        if (p < p1) {
+          const int64_t oi = oi_first + p;
+          int64_t a_lo = 0, a_hi = kh - 1;
+          if (conv) {
+            a_lo = oi - (IH - 1) > 0 ? oi - (IH - 1) : 0;
+            a_hi = oi < kh - 1 ? oi : kh - 1;
+          }
+          double y[CGB_RC];
+          if (sep)
+            strip_rowpass(kw, tb, taps, y, lane);
+          else
+            strip_row(L, oi, a_lo, a_hi, tma ? x + clo : nullptr, IW, ring, SLOT, NS, taps, tb,
+                      y, lane);
+          // the tile of output row p, columns [oj0, oj0 + nvalid): every term
+          // in order, the strip term from y
+          const int64_t row0 = rb.row_begin + p * OW + oj0;
+          double acc[CGB_RC];
+#pragma unroll
+          for (int r = 0; r < CGB_RC; ++r) acc[r] = 0.0;
+          for (int t = rb.term_begin; t < rb.term_end; ++t) {
+            const cgb_term tt = P.terms[t];
+            if (t == rb.strip_term) {
+              tile_transpose(y, os, acc, tt.alpha, nvalid, lane);
+              continue;
+            }
+            const cgb_leaf LL = P.leaves[tt.leaf];
+            const InVec tin = tt.in_buf == 0
+                                  ? in.shift(tt.in_off)
+                                  : InVec{temp + P.temp_off[tt.in_buf - 1] + tt.in_off, nullptr,
+                                          0.0};
+            leaf_tile<false>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
+                             nullptr, nullptr, os, nullptr, 0);
+          }
+          if (rb.out_buf == 0) {
+            epi.tile(row0 + lane, row0, CGB_RC, nvalid - lane, acc, part);
+          } else {
+            double* dst = P.temp[ts] + P.temp_off[rb.out_buf - 1] + row0 + lane;
+#pragma unroll
+            for (int r = 0; r < CGB_RC; ++r)
+              if (lane + 32 * r < nvalid) dst[32 * r] = acc[r];
+          }
+        }
+        __syncthreads();               // every warp is done with step st's rows
+        if (tma && threadIdx.x == 0 && st + 2 < nsteps) issue(st + 2);
+      }
+    }
+  }
+  if (any) __syncthreads();            // the ring overlays the per-warp buffers
+  return any;
+}
+
 // Execute one level of a plan with temporary set `ts`.  Tiles are dealt
 // round-robin across blocks first (tile t -> block t mod G) so every SM
 // streams a similar share.  A warp's conv windows are double buffered: the
@@ -867,6 +1219,7 @@ template <bool WITH2D, class Epi>
 __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
                           double* part) {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
+  const bool strips = run_strips<WITH2D>(P, e, in, ts, epi, part);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* xsb0 = cgb_dyn_smem + (size_t)wib * P.smem_per_warp;
   double* xsb1 = xsb0 + P.smem_xs;
@@ -911,6 +1264,14 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       tile_rows<WITH2D>(nrb, ntile, nrow0, nnvalid);
       nwin = conv_window(P, nrb, nrow0, in, temp);
       if (nwin.ok) issue_window(nwin, cur ? xsb0 : xsb1, &bar[cur ^ 1], lane);
+    }
+    if (strips && rb.strip_term >= 0) {  // done by run_strips
+      cur ^= 1;
+      rbi = nrbi;
+      row0 = nrow0;
+      nvalid = nnvalid;
+      win = nwin;
+      continue;
     }
     double acc[CGB_RC];
 #pragma unroll

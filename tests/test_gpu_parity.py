@@ -333,6 +333,50 @@ def test_conv2d_tiled_against_oracle(h, w, kh, kw):
                                atol=1e-12 * np.abs(a).max())
 
 
+@pytest.mark.parametrize("h,w,kh,kw,kind", [(50, 700, 15, 15, "gauss"), (33, 611, 5, 7, "outer"),
+                                             (20, 300, 1, 15, "outer"), (17, 1200, 15, 1, "outer"),
+                                             (9, 289, 3, 3, "gauss"), (40, 2000, 31, 63, "outer")])
+def test_conv2d_separable_against_oracle(h, w, kh, kw, kind):
+    """Rank-one 2-d kernels take the column-pass + row-pass tile path
+    (CGB_LEAF_FLAG_SEPARABLE): forward and adjoint vs the oracle's scipy
+    convolution at 1e-12, and vs the direct kh x kw path (CGB_NO_SEPARABLE)
+    at 1e-13."""
+    import os
+    from oracle import linop_ref
+    from paper_1609_03488_b200 import _plan, canon
+    import _exprs as E
+    rng = np.random.default_rng(h * 7 + w)
+    K = (canon.gaussian_kernel2d(kh, kw) if kind == "gauss" else
+         np.outer(rng.standard_normal(kh), rng.standard_normal(kw)))
+    assert _plan.separable(K)
+    op = linop.conv2d(K, (h, w))
+    ref = E.Conv2D(K, (h, w))
+    x = rng.standard_normal(h * w)
+    y = rng.standard_normal(op.rows)
+    f, a = op.forward(x), op.adjoint_apply(y)
+    np.testing.assert_allclose(f, linop_ref.forward(ref, x), rtol=1e-12,
+                               atol=1e-12 * np.abs(f).max())
+    np.testing.assert_allclose(a, linop_ref.adjoint(ref, y), rtol=1e-12,
+                               atol=1e-12 * np.abs(a).max())
+    os.environ["CGB_NO_SEPARABLE"] = "1"
+    try:
+        op2 = linop.conv2d(K, (h, w))
+        f2, a2 = op2.forward(x), op2.adjoint_apply(y)
+    finally:
+        del os.environ["CGB_NO_SEPARABLE"]
+    np.testing.assert_allclose(f, f2, rtol=1e-13, atol=1e-13 * np.abs(f).max())
+    np.testing.assert_allclose(a, a2, rtol=1e-13, atol=1e-13 * np.abs(a).max())
+
+
+def test_conv2d_rank_two_kernel_is_not_separable():
+    from paper_1609_03488_b200 import _plan
+    rng = np.random.default_rng(3)
+    K = np.outer(rng.standard_normal(5), rng.standard_normal(5))
+    K += 1e-6 * np.outer(rng.standard_normal(5), rng.standard_normal(5))
+    assert not _plan.separable(K)
+    assert _plan.separable(K[:1]) and _plan.separable(K[:, :1])
+
+
 def test_deconv2d_end_to_end_matches_oracle():
     """configs[2] at small scale: 2-d nonnegative deconvolution of a 40 x 330
     image with a 7 x 7 blur, stuffed like build_deconv, device vs oracle:
