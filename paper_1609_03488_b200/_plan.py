@@ -38,6 +38,7 @@ def _scaled_identity(e) -> float | None:
 
 
 SEPARABLE_KMAX = 63   # CGB_SEP_KMAX
+CONV_KMAX = 240       # CGB_CONV_KMAX: longest 1-d kernel of the tiled conv path
 
 
 def separable(kernel: np.ndarray) -> bool:
@@ -266,6 +267,9 @@ class _Builder:
         if isinstance(e, L.DenseMatrix) and self._emit_split_dense(e, adj, in_buf, in_off,
                                                                    out_buf, out_row, alpha, level):
             return
+        if isinstance(e, L.Conv1D) and len(e.kernel) > CONV_KMAX:
+            self._emit_split_conv(e, adj, in_buf, in_off, out_buf, out_row, alpha, level)
+            return
         li = self.leaf(e, adj)
         self.terms.append((li, in_buf, out_row, in_off, float(alpha), out_buf))
 
@@ -304,6 +308,27 @@ class _Builder:
         for k in range(nsplit):
             self.terms.append((ident, t, out_row, k * rows, float(alpha), out_buf))
         return True
+
+    # long 1-d kernels (the reference's own deconvolution family uses
+    # kernel length n; it switches to FFT above 512 taps, linop.py:35-50):
+    # the taps are cut into blocks of <= CONV_KMAX, each an ordinary tiled
+    # conv leaf, and the blocks' contributions are summed by the row block's
+    # term list (deterministic order, no atomics):
+    #   full conv   y[i]  = sum_b conv(c_b, x)[i - j_b]      (output shift j_b)
+    #   valid corr  y[i]  = sum_b corr(c_b, x[j_b:])[i]       (input shift j_b)
+    def _emit_split_conv(self, e, adj, in_buf, in_off, out_buf, out_row, alpha, level):
+        k, n = len(e.kernel), e.n
+        nblk = -(-k // CONV_KMAX)
+        blk = -(-k // nblk)
+        parts = e.__dict__.setdefault("_cgb_tap_blocks", {})
+        for j0 in range(0, k, blk):
+            sub = parts.get(j0)
+            if sub is None:
+                sub = parts[j0] = L.Conv1D(e.kernel[j0:j0 + blk], n)
+            if adj:
+                self.emit(sub, True, in_buf, in_off + j0, out_buf, out_row, alpha, level)
+            else:
+                self.emit(sub, False, in_buf, in_off, out_buf, out_row + j0, alpha, level)
 
     def finish(self, in_len: int, out_len: int):
         buf_len = [out_len] + self.temp_len

@@ -272,8 +272,13 @@ struct GridSync {
   double* partials;  // [2 banks][CGB_MAXP][grid]
   int bank;
   unsigned long long target;
+  bool cluster;      // the grid is ONE thread-block cluster (small problems)
 
-  __device__ GridSync(GridBar* b, double* p) : bar(b), partials(p), bank(0), target(0) {}
+  __device__ GridSync(GridBar* b, double* p) : bar(b), partials(p), bank(0), target(0) {
+    unsigned n;
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+    cluster = n > 1 && n == gridDim.x;
+  }
 
   // All threads of all blocks must call this (uniform control flow).
   // FENCE selects the ordering around the arrival: 2 = fence.sc before and
@@ -283,6 +288,13 @@ struct GridSync {
   // release / acquire are cumulative over what thread 0 has observed).
   template <int FENCE = CGB_BAR_FENCE>
   __device__ void sync() {
+    if (cluster) {
+      // launched as one cluster: the hardware cluster barrier (release /
+      // acquire at cluster scope orders the global-memory phases too)
+      asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                   "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      return;
+    }
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {

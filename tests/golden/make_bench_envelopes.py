@@ -142,9 +142,18 @@ def b_digest(b: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(b, dtype=np.float64).tobytes()).hexdigest()[:16]
 
 
+# Perturbation size.  4 ulp (seeds 0..99) is the golden-case convention; the
+# device's summation order moves the FIRST iterate by ~6e-12 relative
+# (tools/diverge_bench.py on lasso_dense: 6.3e-12 at k = 1), so envelopes
+# are also measured at REL = 1e-11 (seeds 100..), the perturbation size the
+# device's rounding actually applies -- the 4-ulp family understates it.
+REL = float(os.environ.get("ENVELOPE_REL", "0")) or 4 * ULP
+SEED0 = 100 if REL > 8 * ULP else 0
+
+
 def perturb(v: np.ndarray, seed: int) -> np.ndarray:
     rng = np.random.default_rng(1000 + seed)
-    return v * (1.0 + 4 * ULP * rng.uniform(-1, 1, v.shape))
+    return v * (1.0 + REL * rng.uniform(-1, 1, v.shape))
 
 
 def _solve_job(name: str, seed: int) -> dict:
@@ -154,7 +163,7 @@ def _solve_job(name: str, seed: int) -> dict:
     digest = b_digest(b)
     if seed >= 0:
         rng_b = perturb(b, seed)
-        c = c * (1.0 + 4 * ULP * np.random.default_rng(2000 + seed).uniform(-1, 1, c.shape))
+        c = c * (1.0 + REL * np.random.default_rng(2000 + seed).uniform(-1, 1, c.shape))
         b = rng_b
     t0 = time.time()
     if solver == "reference":
@@ -181,7 +190,8 @@ def _solve_job(name: str, seed: int) -> dict:
             "status": sol.status, "iterations": int(sol.iterations), "pobj": float(sol.pobj),
             "dobj": float(sol.dobj), "avg_cg": float(sol.avg_cg_iterations),
             "seconds": time.time() - t0,
-            "perturbation": "none" if seed < 0 else "b, c *= 1 + U(-4, 4) ulp"}
+            "perturbation": "none" if seed < 0 else (
+                "b, c *= 1 + U(-4, 4) ulp" if REL <= 8 * ULP else f"b, c *= 1 + U(-{REL:g}, {REL:g})")}
 
 
 def _worker_init():
@@ -204,7 +214,8 @@ def main(names=None):
     workers = int(os.environ.get("ENVELOPE_WORKERS", "6"))
     names = names or list(INSTANCES)
     have = done_jobs()
-    jobs = [(nm, s) for nm in names for s in range(-1, min(seeds, INSTANCES[nm][2]))
+    jobs = [(nm, s) for nm in names
+            for s in [-1] + list(range(SEED0, SEED0 + min(seeds, INSTANCES[nm][2])))
             if (nm, s) not in have]
     print(f"{len(jobs)} solves to run on {workers} workers", flush=True)
     with ProcessPoolExecutor(max_workers=workers, initializer=_worker_init) as ex:

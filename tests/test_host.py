@@ -210,3 +210,22 @@ def test_oracle_stuffing_matches_product(name, kw):
     y = rng.standard_normal(pp.A.rows)
     np.testing.assert_array_equal(linop_ref.forward(pp.A.expr, x), linop_ref.forward(po.A, x))
     np.testing.assert_array_equal(linop_ref.adjoint(pp.A.expr, y), linop_ref.adjoint(po.A, y))
+
+
+def test_long_conv_kernel_lowered_to_tap_blocks(monkeypatch):
+    """A Conv1D longer than the tiled path's 240 taps is lowered to tap
+    blocks of <= 240 (plan lowering only; leaf data kept on the host)."""
+    import numpy as np
+    import torch
+    from paper_1609_03488_b200 import _plan
+    from paper_1609_03488_b200 import linop as L
+    monkeypatch.setattr(_plan, "_cuda", lambda a, dtype=None: torch.from_numpy(
+        np.ascontiguousarray(a if dtype is None else a.astype(dtype))))
+    e = L.Conv1D(np.ones(10001), 10001)
+    for adj in (False, True):
+        b = _plan._Builder()
+        b.emit(e, adj, 0, 0, 0, 0, 1.0, 0)
+        ks = [b.leaves[t[0]].k0 for t in b.terms]
+        assert len(ks) == 42 and max(ks) <= _plan.CONV_KMAX and sum(ks) == 10001
+        offs = sorted((t[3] if adj else t[2]) for t in b.terms)
+        assert offs[0] == 0 and offs[-1] == 10001 - ks[-1]
