@@ -1006,12 +1006,23 @@ static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t bas
   const bool conv = L.kind == CGB_LEAF_CONV2D;
   const int kh = (int)L.k0;
   const int s0 = (int)(((base0 % NS) + NS) % NS);
-  auto X = [&](int i, int c) -> double {
+  // shared-memory offset of every row the step reads (kh + 7 of them, at
+  // most CGB_SEP_KMAX + 7), -1 for rows outside the image: computed once,
+  // so the column loop's loads are one add + one shared load each
+  constexpr int kMaxRows = 64 + CGB_WARPS;
+  __shared__ int32_t roff_s[kMaxRows];
+  for (int i = threadIdx.x; i < kh + CGB_WARPS; i += blockDim.x) {
     const int64_t r = base0 + i;
     const int slot = s0 + i >= NS ? s0 + i - NS : s0 + i;
     const int sh = (sh0 + (shodd & (int)(r & 1))) & 1;
-    const double v = ring[(size_t)slot * SLOT + sh + c];
-    return (r >= 0 && r < IH) ? v : 0.0;
+    roff_s[i] = (r >= 0 && r < IH) ? slot * SLOT + sh : -1;
+  }
+  __syncthreads();
+  const double* sring = ring;
+  auto X = [&](int i, int c) -> double {
+    const int o = roff_s[i];
+    const double v = sring[(o < 0 ? 0 : o) + c];
+    return o < 0 ? 0.0 : v;
   };
   for (int c = threadIdx.x; c < span; c += blockDim.x) {
     double acc[CGB_WARPS], xw[CGB_WARPS];
@@ -1075,6 +1086,17 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
   double* os = ring + (size_t)NS * SLOT + (size_t)wib * (SLOT + 32 * CGB_RC + 2);
   double* tb = os + 32 * CGB_RC + 2;
   bool any = false;
+  // timeline probe (profiling only): thread 0 of block 0 adds ns to
+  // cgb_tl_acc[8..15]: 8 batch wait, 9 column pass, 10 its barrier, 11 row
+  // pass + other terms + epilogue, 12 step barrier, 13 steps, 14 tasks
+  double* tl = (blockIdx.x == 0 && threadIdx.x == 0) ? cgb_tl_acc : nullptr;
+  uint64_t tl1 = tl ? globaltimer() : 0;
+#define CGB_TL(slot)                                      \
+  if (tl) {                                                \
+    const uint64_t tl_x = globaltimer();                   \
+    tl[slot] += (double)(tl_x - tl1);                      \
+    tl1 = tl_x;                                            \
+  }
   for (int rbi = rb_lo; rbi < rb_hi; ++rbi) {
     const DevRowBlock rb = P.rbs[rbi];
     if (rb.strip_term < 0) continue;
@@ -1147,7 +1169,10 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
         issue(0);
         if (nsteps > 1) issue(1);
       }
+      if (tl) tl[14] += 1.0;
+      CGB_TL(12)
       for (int st = 0; st < nsteps; ++st) {
+        if (tl) tl[13] += 1.0;
         if (tma) {
           const uint32_t g = base + st;
           mbar_wait(&cgb_strip_mbar[g & 1u], (g >> 1) & 1u);
@@ -1158,6 +1183,7 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
             stage_row(x + r * IW, clo, IW, span, ring + (size_t)(r % NS) * SLOT, lane);
           __syncthreads();
         }
+        CGB_TL(8)
         const int64_t p = p0 + (int64_t)CGB_WARPS * st + wib;
         if (sep) {
           // all threads: column sums of the step's 8 output rows
@@ -1166,7 +1192,9 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
           strip_colpass(L, conv ? o0 - (kh - 1) : o0, IH, span, ring, SLOT, NS, sh0,
                         tma ? (int)(IW & 1) : 0, taps + ntaps,
                         ring + (size_t)NS * SLOT + 32 * CGB_RC + 2, SLOT + 32 * CGB_RC + 2);
+          CGB_TL(9)
           __syncthreads();
+          CGB_TL(10)
         }
         if (p < p1) {
           const int64_t oi = oi_first + p;
@@ -1210,12 +1238,15 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
               if (lane + 32 * r < nvalid) dst[32 * r] = acc[r];
           }
         }
+        CGB_TL(11)
         __syncthreads();               // every warp is done with step st's rows
         if (tma && threadIdx.x == 0 && st + 2 < nsteps) issue(st + 2);
+        CGB_TL(12)
       }
     }
   }
   if (any) __syncthreads();            // the ring overlays the per-warp buffers
+#undef CGB_TL
   return any;
 }
 

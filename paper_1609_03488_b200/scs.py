@@ -329,7 +329,7 @@ class SolverPlan:
         """Accumulate per-phase device time of later run() calls (ns)."""
         import torch
         if on:
-            self._prof = torch.zeros(32, dtype=torch.float64, device="cuda")
+            self._prof = torch.zeros(48, dtype=torch.float64, device="cuda")
             ptr = _lib.ptr(self._prof)
         else:
             self._prof = None
@@ -344,6 +344,12 @@ class SolverPlan:
         out["rhs_warp0_timeline"] = {"tiles": float(tl[0] * 1e9), "tma_wait": float(tl[1]),
                                      "conv": float(tl[2]), "other_terms": float(tl[3]),
                                      "epilogue": float(tl[4]), "level_total": float(tl[5])}
+        sv = vals[24:32]
+        out["rhs_strip_timeline"] = {"batch_wait": float(sv[0]), "colpass": float(sv[1]),
+                                     "colpass_barrier": float(sv[2]),
+                                     "rowpass_terms_epilogue": float(sv[3]),
+                                     "step_barrier_issue": float(sv[4]),
+                                     "steps": float(sv[5] * 1e9), "tasks": float(sv[6] * 1e9)}
         return out
 
     def loop_vars(self) -> list:
