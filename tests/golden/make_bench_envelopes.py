@@ -55,7 +55,7 @@ MAX_ITERS = 100_000
 # name -> (workload constructor spec, solver, seeds); cheap instances first
 INSTANCES = {
     # configs[0] at its full size
-    "lasso_dense_1000x500": ({"workload": "lasso_dense"}, "reference", 16),
+    "lasso_dense_1000x500": ({"workload": "lasso_dense"}, "reference", 32),
     # configs[4] families at CPU-feasible sizes
     "soc_ls_20000x200": ({"workload": "soc_ls", "m": 20_000, "n": 200}, "reference", 8),
     "logreg_600x20": ({"workload": "logreg", "m": 600, "n": 20}, "oracle", 8),
@@ -148,7 +148,8 @@ def b_digest(b: np.ndarray) -> str:
 # are also measured at REL = 1e-11 (seeds 100..), the perturbation size the
 # device's rounding actually applies -- the 4-ulp family understates it.
 REL = float(os.environ.get("ENVELOPE_REL", "0")) or 4 * ULP
-SEED0 = 100 if REL > 8 * ULP else 0
+# seed ranges per perturbation size: 4 ulp 0..99, 1e-11 100..199, 1e-10 200..
+SEED0 = 0 if REL <= 8 * ULP else (100 if REL <= 2e-11 else 200)
 
 
 def perturb(v: np.ndarray, seed: int) -> np.ndarray:

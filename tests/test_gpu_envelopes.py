@@ -4,8 +4,15 @@ tests/golden/bench_envelopes.jsonl holds, for members of every BASELINE
 config's family at CPU-feasible sizes (configs[0] at its full size), the
 REAL reference's solve (or the pinned oracle's, for the north-star
 extensions the reference lacks: 2-d convolution, exponential cones) of the
-unperturbed instance and of copies with b, c perturbed by <= 4 ulp
-(tests/golden/make_bench_envelopes.py).  The device solve of the same
+unperturbed instance and of copies with b, c multiplied by 1 + U(-d, d)
+for d = 4 ulp, 1e-11 and (configs[0]) 1e-10 (tests/golden/
+make_bench_envelopes.py).  Why the larger d: the device's summation order
+moves the first iterate by ~6e-12 relative (tools/diverge_bench.py) and
+the splitting map amplifies it; on configs[0] the device's own counts over
+reduction orders (grid sizes 37..148, 1..4 sharded ranks:
+tools/grid_spread.py) are {760, 780, 840, 920}, and the reference's counts
+under d = 1e-10 are {740, 760, 780, 840, 920} -- the same distribution,
+which a 4-ulp envelope ({840}) does not show.  The device solve of the same
 instance (rebuilt from the same host-side generator, digest-checked) must
 satisfy the north-star rule against that envelope:
 
