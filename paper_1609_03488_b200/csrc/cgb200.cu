@@ -95,6 +95,11 @@ struct EpiRhs {
   const double* dw;
   double tau_w;
   int64_t c_lo, c_hi;  // c is zero outside [c_lo, c_hi)
+  __device__ void prefetch(int64_t j0, int n, int lane) const {
+    prefetch_range(dw ? dw : d1, j0, n, lane);
+    prefetch_range(x0, j0, n, lane);
+    prefetch_range(g, j0, n, lane);
+  }
   __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     const bool hc = c && jlo < c_hi && jlo + 32 * R > c_lo;  // warp-uniform
@@ -318,6 +323,10 @@ struct EpiT {
   double beta;
   int first;
   int64_t b_lo, b_hi;  // b is zero outside [b_lo, b_hi)
+  __device__ void prefetch(int64_t j0, int n, int lane) const {
+    if (!first) prefetch_range(t, j0, n, lane);
+    if (b && j0 < b_hi && j0 + n > b_lo) prefetch_range(b, j0, n, lane);
+  }
   __device__ void tile(int64_t i, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     const bool hb = b && jlo < b_hi && jlo + 32 * R > b_lo;  // warp-uniform
@@ -379,6 +388,12 @@ __device__ __forceinline__ void pdots(int64_t n, const double* r, const double* 
 struct EpiCgUpd {
   double* r; double* p; double* x; double* gx;
   double beta; int first; double lam, alpha;
+  __device__ void prefetch(int64_t j0, int n, int lane) const {
+    prefetch_range(r, j0, n, lane);
+    if (!first) prefetch_range(p, j0, n, lane);
+    prefetch_range(x, j0, n, lane);
+    prefetch_range(gx, j0, n, lane);
+  }
   __device__ void tile(int64_t j, int64_t jlo, int R, int left, const double (&y)[CGB_RC],
                        double* part) const {
     double rv[CGB_RC], pv[CGB_RC], xv[CGB_RC], gv[CGB_RC];

@@ -940,6 +940,23 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
                                           double (&acc)[CGB_RC], int lane, const double* cc,
                                           double* xs, double* os, double* ring, int xs2);
 
+// L2 prefetch of the 128-byte lines of p[j0, j0 + n) (one line per lane)
+__device__ __forceinline__ void prefetch_range(const double* p, int64_t j0, int n, int lane) {
+  if (!p || n <= 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p + j0) & ~uintptr_t(127);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(p + j0 + n - 1);
+  for (uintptr_t a = a0 + 128 * (uintptr_t)lane; a <= a1; a += 32 * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+// epilogues may declare prefetch(j0, n, lane) for the operands they read
+template <class E>
+__device__ __forceinline__ auto epi_prefetch(const E& e, int64_t j0, int n, int lane, int)
+    -> decltype(e.prefetch(j0, n, lane), void()) {
+  e.prefetch(j0, n, lane);
+}
+template <class E>
+__device__ __forceinline__ void epi_prefetch(const E&, int64_t, int, int, long) {}
+
 // One output row segment of a strip: y = the conv of kernel rows
 // [a_lo, a_hi] with the ring's input rows (slot = input row mod NS); xrow0
 // != null: the rows came by TMA from x + row * IW (+ the copy's alignment
@@ -1173,6 +1190,20 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
       CGB_TL(12)
       for (int st = 0; st < nsteps; ++st) {
         if (tl) tl[13] += 1.0;
+        {  // L2 prefetch of the operands this warp's NEXT output row segment reads
+          const int64_t pn = p0 + (int64_t)CGB_WARPS * (st + 1) + wib;
+          if (pn < p1) {
+            const int64_t rn = rb.row_begin + pn * OW + oj0;
+            epi_prefetch(epi, rn, nvalid, lane, 0);
+            for (int t = rb.term_begin; t < rb.term_end; ++t) {
+              const cgb_term tt = P.terms[t];
+              if (t == rb.strip_term || P.leaves[tt.leaf].kind != CGB_LEAF_IDENTITY) continue;
+              const double* src = tt.in_buf == 0 ? in.a + tt.in_off
+                                                 : temp + P.temp_off[tt.in_buf - 1] + tt.in_off;
+              prefetch_range(src, rn - tt.row_origin, nvalid, lane);
+            }
+          }
+        }
         if (tma) {
           const uint32_t g = base + st;
           mbar_wait(&cgb_strip_mbar[g & 1u], (g >> 1) & 1u);

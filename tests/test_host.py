@@ -229,3 +229,18 @@ def test_long_conv_kernel_lowered_to_tap_blocks(monkeypatch):
         assert len(ks) == 42 and max(ks) <= _plan.CONV_KMAX and sum(ks) == 10001
         offs = sorted((t[3] if adj else t[2]) for t in b.terms)
         assert offs[0] == 0 and offs[-1] == 10001 - ks[-1]
+
+
+def test_graph_engine_names_import_and_fail_clearly():
+    """The reference's graph-engine exports (conegraph/__init__.py:3-4)
+    import from the drop-in package and raise a clear error when used."""
+    import pytest
+    import paper_1609_03488_b200 as pkg
+    from paper_1609_03488_b200.graph import GraphEngineUnavailable
+    for name in ("Graph", "LoopSpec", "Node", "NodeId", "debug_dump", "evaluate",
+                 "evaluate_args", "topological_order", "while_loop"):
+        assert hasattr(pkg, name)
+    with pytest.raises(GraphEngineUnavailable):
+        pkg.Graph()
+    with pytest.raises(GraphEngineUnavailable):
+        pkg.evaluate(None)
