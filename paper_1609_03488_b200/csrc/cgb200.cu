@@ -1701,14 +1701,15 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       const cgb_leaf& LF = leaves[d->terms[t2].leaf];
       const int64_t nt = (LF.k1 + CGB_RC - 1) / CGB_RC * CGB_RC;
       const int64_t slot = (32 * CGB_RC + nt + 2 + 1) & ~1;
-      const int64_t need = (LF.k0 + 15) * slot + CGB_WARPS * (slot + 32 * CGB_RC + 2);
+      const int64_t need = (LF.k0 + 15) * slot + CGB_WARPS * (2 * slot + 32 * CGB_RC + 2);
       if (need > 24 * 1024) continue;  // 192 KB of shared memory at most
       D.strip_term = t2;
       khmax = std::max<int64_t>(khmax, LF.k0);
       ntmax = std::max<int64_t>(ntmax, nt);
     }
     const int64_t slot_all = (32 * CGB_RC + ntmax + 2 + 1) & ~1;
-    if (khmax > 0 && (khmax + 15) * slot_all + CGB_WARPS * (slot_all + 32 * CGB_RC + 2) > 24 * 1024) {
+    if (khmax > 0 &&
+        (khmax + 15) * slot_all + CGB_WARPS * (2 * slot_all + 32 * CGB_RC + 2) > 24 * 1024) {
       for (DevRowBlock& D : rbs) D.strip_term = -1;   // several kernels: over budget together
       khmax = 0;
     }
@@ -1773,7 +1774,8 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   P.smem_total = CGB_WARPS * P.smem_per_warp;
   if (P.strip_rows > 0)
     P.smem_total = std::max<int32_t>(
-        P.smem_total, P.strip_nslot * P.strip_slot + CGB_WARPS * (P.strip_slot + 32 * CGB_RC + 2));
+        P.smem_total,
+        P.strip_nslot * P.strip_slot + CGB_WARPS * (2 * P.strip_slot + 32 * CGB_RC + 2));
   P.in_len = d->in_len;
   P.out_len = d->out_len;
   ps->in_len = d->in_len;

@@ -1041,28 +1041,43 @@ static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t bas
     const double v = sring[(o < 0 ? 0 : o) + c];
     return o < 0 ? 0.0 : v;
   };
-  for (int c = threadIdx.x; c < span; c += blockDim.x) {
-    double acc[CGB_WARPS], xw[CGB_WARPS];
+  // a thread owns column c and, when the window is wider than the CTA,
+  // column c + blockDim.x too: both run interleaved in one loop (two
+  // independent FMA chains per row hide the shared-load latency) instead of
+  // one after the other, which doubled the step time of the first warps
+  const int c0 = threadIdx.x, c1 = threadIdx.x + blockDim.x;
+  const bool two = c1 < span;
+  if (c0 >= span) return;
+  const int c1s = two ? c1 : c0;
+  double acc0[CGB_WARPS], xw0[CGB_WARPS], acc1[CGB_WARPS], xw1[CGB_WARPS];
 #pragma unroll
-    for (int j = 0; j < CGB_WARPS; ++j) {
-      acc[j] = 0.0;
-      xw[j] = X(j, c);
-    }
-    for (int g = 0; g < (kh + CGB_WARPS - 1) / CGB_WARPS; ++g) {
+  for (int j = 0; j < CGB_WARPS; ++j) {
+    acc0[j] = acc1[j] = 0.0;
+    xw0[j] = X(j, c0);
+    xw1[j] = X(j, c1s);
+  }
+  for (int g = 0; g < (kh + CGB_WARPS - 1) / CGB_WARPS; ++g) {
 #pragma unroll
-      for (int jj = 0; jj < CGB_WARPS; ++jj) {
-        const int a = CGB_WARPS * g + jj;
-        if (a < kh) {
-          const double wa = u[conv ? kh - 1 - a : a];
+    for (int jj = 0; jj < CGB_WARPS; ++jj) {
+      const int a = CGB_WARPS * g + jj;
+      if (a < kh) {
+        const double wa = u[conv ? kh - 1 - a : a];
 #pragma unroll
-          for (int j = 0; j < CGB_WARPS; ++j)
-            acc[j] = fma(wa, xw[(jj + j) % CGB_WARPS], acc[j]);
-          if (a + 1 < kh) xw[jj] = X(a + CGB_WARPS, c);  // slot jj: row a -> row a + 8
+        for (int j = 0; j < CGB_WARPS; ++j) {
+          acc0[j] = fma(wa, xw0[(jj + j) % CGB_WARPS], acc0[j]);
+          acc1[j] = fma(wa, xw1[(jj + j) % CGB_WARPS], acc1[j]);
+        }
+        if (a + 1 < kh) {                       // slot jj: row a -> row a + 8
+          xw0[jj] = X(a + CGB_WARPS, c0);
+          xw1[jj] = X(a + CGB_WARPS, c1s);
         }
       }
     }
+  }
 #pragma unroll
-    for (int j = 0; j < CGB_WARPS; ++j) tbase[(size_t)j * tstride + c] = acc[j];
+  for (int j = 0; j < CGB_WARPS; ++j) {
+    tbase[(size_t)j * tstride + c0] = acc0[j];
+    if (two) tbase[(size_t)j * tstride + c1] = acc1[j];
   }
 }
 
@@ -1100,8 +1115,11 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
   const double* temp = P.temp[ts];
   const int SLOT = P.strip_slot, NS = P.strip_nslot;
   double* ring = cgb_dyn_smem;
-  double* os = ring + (size_t)NS * SLOT + (size_t)wib * (SLOT + 32 * CGB_RC + 2);
-  double* tb = os + 32 * CGB_RC + 2;
+  // per warp: transpose buffer | two t buffers (separable strips alternate
+  // them, so a step needs only the barrier after its column pass)
+  const int WSTRIDE = 2 * SLOT + 32 * CGB_RC + 2;
+  double* os = ring + (size_t)NS * SLOT + (size_t)wib * WSTRIDE;
+  const unsigned issuer = blockDim.x - 32;  // lane 0 of the last warp (one column)
   bool any = false;
   // timeline probe (profiling only): thread 0 of block 0 adds ns to
   // cgb_tl_acc[8..15]: 8 batch wait, 9 column pass, 10 its barrier, 11 row
@@ -1182,7 +1200,7 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
         }
         cgb_strip_seq = base + st + 1;
       };
-      if (tma && threadIdx.x == 0) {
+      if (tma && threadIdx.x == issuer) {
         issue(0);
         if (nsteps > 1) issue(1);
       }
@@ -1216,15 +1234,19 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
         }
         CGB_TL(8)
         const int64_t p = p0 + (int64_t)CGB_WARPS * st + wib;
+        double* tb = os + 32 * CGB_RC + 2 + (st & 1) * SLOT;
         if (sep) {
           // all threads: column sums of the step's 8 output rows
           const int64_t o0 = oi_first + p0 + (int64_t)CGB_WARPS * st;
           const int sh0 = tma ? (int)((reinterpret_cast<uintptr_t>(x + clo) >> 3) & 1) : 0;
           strip_colpass(L, conv ? o0 - (kh - 1) : o0, IH, span, ring, SLOT, NS, sh0,
                         tma ? (int)(IW & 1) : 0, taps + ntaps,
-                        ring + (size_t)NS * SLOT + 32 * CGB_RC + 2, SLOT + 32 * CGB_RC + 2);
+                        ring + (size_t)NS * SLOT + 32 * CGB_RC + 2 + (st & 1) * SLOT, WSTRIDE);
           CGB_TL(9)
           __syncthreads();
+          // the rows only this step read are free: batch st + 2 goes now,
+          // under the row passes
+          if (tma && threadIdx.x == issuer && st + 2 < nsteps) issue(st + 2);
           CGB_TL(10)
         }
         if (p < p1) {
@@ -1270,8 +1292,10 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
           }
         }
         CGB_TL(11)
-        __syncthreads();               // every warp is done with step st's rows
-        if (tma && threadIdx.x == 0 && st + 2 < nsteps) issue(st + 2);
+        if (!sep) {
+          __syncthreads();             // every warp is done with step st's rows
+          if (tma && threadIdx.x == issuer && st + 2 < nsteps) issue(st + 2);
+        }
         CGB_TL(12)
       }
     }
