@@ -56,14 +56,6 @@ def separable(kernel: np.ndarray) -> bool:
     return len(s) < 2 or s[1] <= 1e-13 * s[0]
 
 
-def decouple_conv2d() -> bool:
-    """Conv2D leaves go through a temporary (see _Builder.emit); the
-    CGB_CONV2D_FUSED=1 environment variable keeps them fused in the
-    output block (A/B)."""
-    import os
-    return not os.environ.get("CGB_CONV2D_FUSED")
-
-
 def _cuda(a: np.ndarray, dtype=None):
     import torch
     t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else a.astype(dtype)))
@@ -139,7 +131,6 @@ class _Builder:
         self.temp_level: list[int] = []
         self.keep: list = []
         self.leaf_nnz: dict[int, int] = {}  # CSR leaf index -> nnz (roofline bytes)
-        self.decoupled: set[int] = set()    # temporaries of decouple_conv2d (not algorithmic)
 
     # -- leaves -------------------------------------------------------------
     def _add_leaf(self, key, make):
@@ -278,19 +269,6 @@ class _Builder:
             return
         if isinstance(e, L.Conv1D) and len(e.kernel) > CONV_KMAX:
             self._emit_split_conv(e, adj, in_buf, in_off, out_buf, out_row, alpha, level)
-            return
-        if isinstance(e, L.Conv2D) and decouple_conv2d():
-            # the 2-d convolution into its own temporary one level deeper (a
-            # block of CTA strips that only store), summed into the output by
-            # an identity term: the block's other terms and the fused
-            # epilogue then run as plain streaming tiles instead of inside
-            # the strip step's latency chain
-            t = self.new_temp(rows, level + 1)
-            self.decoupled.add(t)
-            self.terms.append((self.leaf(e, adj), in_buf, 0, in_off, 1.0, t))
-            ident = self._add_leaf(("I", rows), lambda: (_lib.Leaf(kind=_lib.LEAF_IDENTITY,
-                                                                   rows=rows, cols=rows), 0))
-            self.terms.append((ident, t, out_row, 0, float(alpha), out_buf))
             return
         li = self.leaf(e, adj)
         self.terms.append((li, in_buf, out_row, in_off, float(alpha), out_buf))
@@ -520,5 +498,4 @@ class DeviceOp:
         total = sum(_leaf_data_bytes(leaf, b.leaf_nnz.get(i, 0))
                     for i, leaf in enumerate(b.leaves))
         n_in, n_out = (self.rows, self.cols) if adjoint else (self.cols, self.rows)
-        temps = sum(n for i, n in enumerate(b.temp_len) if (i + 1) not in b.decoupled)
-        return total + 8 * n_in + 8 * n_out + 16 * temps
+        return total + 8 * n_in + 8 * n_out + 16 * sum(b.temp_len)
