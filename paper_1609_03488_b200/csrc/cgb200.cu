@@ -740,6 +740,7 @@ struct ScsArgs {
   int stash_cap;   // doubles of shared memory per CTA for the SOC stash
   double* prof;    // PROF_N phase times (ns) or null
   int no_skip;     // 1: stream all of b and c (CGB_SCS_NO_ZERO_SKIP)
+  double* park;    // m: large-SOC source between passes A and B (the CG scratch t), or null
 };
 
 // [first, last + 1) of the nonzeros of b (slots 0, 1) and c (slots 2, 3),
@@ -856,6 +857,31 @@ struct SocPassB {
   __device__ __forceinline__ void compute(int64_t i, const double (&v)[1], int64_t j) {
     const double z = stash[j];
     bw += v[0] * cs->store(base + i, z, sc.tail(z));
+  }
+};
+
+// large SOC too big for the shared-memory stash: pass A parks its source in
+// a global scratch vector (the CG scratch t, idle during the cone step) and
+// pass B reads it back with b -- 2 reads instead of recomputing the source
+// from 4 (bitwise the same source value).
+struct SocPassAG {
+  double tau;
+  double* park;  // indexed like the tail
+  double acc;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[4], int64_t) {
+    const double z = ((v[0] + v[1]) - tau * v[2]) - v[3];
+    acc += z * z;
+    park[i] = z;
+  }
+};
+struct SocPassBG {  // inputs: the parked source, b
+  const ConeStep* cs;
+  int64_t base;
+  SocCoef sc;
+  double bw;
+  __device__ __forceinline__ void compute(int64_t i, const double (&v)[2], int64_t) {
+    const double z = v[0];
+    bw += v[1] * cs->store(base + i, z, sc.tail(z));
   }
 };
 
@@ -1053,11 +1079,17 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
         const DevSeg sg = K.seg[sg_i];
         if (sg.kind != SEG_SOC_LARGE) continue;
         const int64_t b0 = sg.begin + 1, len = sg.end - sg.begin - 1;
-        SocPassA f{tau_t, use_stash ? stash_base + so : nullptr, 0.0};
         const double* src[4] = {wy + b0, W.tax + b0, a.g + n + b0, W.v + n + b0};
-        bulk_stream<4>(len, src, f);
+        if (use_stash || !a.park) {
+          SocPassA f{tau_t, use_stash ? stash_base + so : nullptr, 0.0};
+          bulk_stream<4>(len, src, f);
+          red[sg.slot] += f.acc;
+        } else {
+          SocPassAG f{tau_t, a.park + b0, 0.0};
+          bulk_stream<4>(len, src, f);
+          red[sg.slot] += f.acc;
+        }
         so += stream_span(len);
-        red[sg.slot] += f.acc;
         if (blockIdx.x == 0 && threadIdx.x == 0) red[K.nlarge + sg.slot] += cs.src(sg.begin);
       }
     }
@@ -1087,6 +1119,11 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
           SocPassB f{&cs, b0, sc, stash_base + so, 0.0};
           const double* src[1] = {a.b + b0};
           bulk_stream<1>(len, src, f);
+          bw += f.bw;
+        } else if (a.park) {
+          SocPassBG f{&cs, b0, sc, 0.0};
+          const double* src[2] = {a.park + b0, a.b + b0};
+          bulk_stream<2>(len, src, f);
           bw += f.bw;
         } else {
           SocPassB2 f{&cs, b0, sc, 0.0};
@@ -2105,6 +2142,7 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.resid_every = resid_every_iter;
   a.prof = ctx->prof;
   a.no_skip = (prob->flags & CGB_SCS_NO_ZERO_SKIP) ? 1 : 0;
+  a.park = std::getenv("CGB_NO_SOC_PARK") ? nullptr : work->t;
   // shared memory: conv staging of the plans, or the large-SOC stash of the
   // cone step, whichever is larger (never live together; one CTA per SM --
   // the kernel re-checks the stash need with the real grid)
