@@ -366,3 +366,47 @@ def test_shard_solve_matches_reference(name, world):
             spread = max([abs(p - ref) for p in pobjs] + [0.0])
             tol = 2.0 * spread + 10 * st.eps * max(1.0, abs(ref))
         assert abs(sol.pobj - ref) <= tol, (sol.pobj, ref, tol)
+
+
+def _ipc_worker(rank, world, port, name, out):
+    """One rank of a 2-process sharded solve on ONE GPU: the IPC handle
+    exchange, cudaIpcOpenMemHandle'd peer buffers, rank-0 gather."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CGB_GRID="16")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1609_03488_b200 import scs, shard
+        prob, _, meta = _golden_problem(name)
+        sol, rs = shard.solve_sharded(prob, scs.ScsSettings(**meta["settings"]))
+        st = rs.state()
+        out[rank] = (None if sol is None else (sol.status, sol.iterations, float(sol.pobj)),
+                     float(st[0]), float(st[11]))
+        rs.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["scs_lp_equality", "scs_soc_ball"])
+def test_multiprocess_ipc_sharded_solve(name):
+    """shard.solve_sharded as a 2-process torch.distributed job sharing one
+    GPU (the transport of a one-rank-per-GPU run: peer buffers allocated by
+    cgb_ipc_alloc, handles exchanged with all_gather_object, mapped with
+    cgb_ipc_open).  Without MPS the two contexts time-slice the GPU, so the
+    case is tiny; the result must equal the reference's exactly."""
+    import torch.multiprocessing as mp
+    _, _, meta = _golden_problem(name)
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_ipc_worker, args=(world, port, name, out), nprocs=world, join=True)
+        res = dict(out)
+    sol0 = res[0][0]
+    assert sol0 is not None and res[1][0] is None          # gathered on rank 0
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]  # same k, same epoch
+    assert sol0[0] == meta["status"] and sol0[1] == meta["iterations"], (sol0, meta["iterations"])
+    if sol0[0] == "solved":
+        assert abs(sol0[2] - meta["pobj"]) <= 1e-6 * max(1.0, abs(meta["pobj"]))
