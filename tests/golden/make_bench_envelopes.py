@@ -67,7 +67,7 @@ INSTANCES = {
     "deconv2d_40x330_k7": ({"workload": "deconv2d", "h": 40, "w": 330, "k": 7}, "oracle", 8),
     # configs[1] family (kernel 101) at a CPU-feasible size, and the bench instance itself
     "deconv1d_n100000_k101": ({"workload": "deconv1d", "n": 100_000}, "reference", 8),
-    "deconv1d_n1000000_k101": ({"workload": "deconv1d", "n": 1_000_000}, "oracle", 4),
+    "deconv1d_n1000000_k101": ({"workload": "deconv1d", "n": 1_000_000}, "oracle", 5),
 }
 
 

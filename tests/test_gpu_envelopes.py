@@ -38,7 +38,11 @@ MBE = importlib.util.module_from_spec(_spec)
 _spec.loader.exec_module(MBE)
 
 ENV = MBE.load_envelopes()
-NAMES = sorted(n for n, e in ENV.items() if e["unperturbed"] is not None and n in MBE.INSTANCES)
+# an instance is tested once its envelope has the unperturbed solve and at
+# least 3 perturbed ones (the n = 1e6 bench instance's oracle solves take
+# ~2.6 h of CPU each)
+NAMES = sorted(n for n, e in ENV.items()
+               if e["unperturbed"] is not None and len(e["perturbed"]) >= 3 and n in MBE.INSTANCES)
 
 
 def _check(name, sol, settings):
