@@ -160,11 +160,13 @@ def _cuda(a):
 
 @dataclass
 class PrecomputedSolve:
-    """Cached pieces of the (I+Q) solve: h = (c, b), g = (I+Q_z)^{-1} h."""
+    """Cached pieces of the (I+Q) solve: h = (c, b), g = (I+Q_z)^{-1} h.
+    ``h`` and ``g`` are host copies made on first access (the solver uses
+    the device copies; a solve never pays for the transfers)."""
 
     A: Operator
-    h: np.ndarray
-    g: np.ndarray
+    _h: object
+    _g: object
     denom: float
     cg_tol: float
     cg_max_iter: int | None
@@ -172,6 +174,18 @@ class PrecomputedSolve:
     g_device: object = None
     c_device: object = None
     b_device: object = None
+
+    @property
+    def h(self) -> np.ndarray:
+        if callable(self._h):
+            self._h = self._h()
+        return self._h
+
+    @property
+    def g(self) -> np.ndarray:
+        if self._g is None:
+            self._g = self.g_device.cpu().numpy()
+        return self._g
 
 
 def _inner_solve(dev, d1, d2, tol, max_iter, c_dev=None, b_dev=None):
@@ -202,11 +216,10 @@ def prepare_subspace(problem: ConeProblem, cg_tol: float = 1e-12,
     dev = _own_device_op(problem.A)
     c_d, b_d = _cuda(problem.c), _cuda(problem.b)
     z, res, hdot = _inner_solve(dev, c_d, b_d, cg_tol, cg_max_iter, c_d, b_d)
-    h = np.concatenate([problem.c, problem.b])
-    g = z.cpu().numpy()
+    c, b = problem.c, problem.b
     denom = 1.0 + hdot
-    return PrecomputedSolve(problem.A, h, g, denom, cg_tol, cg_max_iter, int(res.iterations),
-                            z, c_d, b_d)
+    return PrecomputedSolve(problem.A, lambda: np.concatenate([c, b]), None, denom, cg_tol,
+                            cg_max_iter, int(res.iterations), z, c_d, b_d)
 
 
 def subspace_project(w, cached: PrecomputedSolve) -> np.ndarray:
@@ -279,10 +292,6 @@ class SolverPlan:
         self.buf["state"] = torch.zeros(_lib.STATE_LEN, **f64)
         self.work = _lib.ScsWorkC(**{nm: t.data_ptr() for nm, t in self.buf.items()})
         ca = self.cached
-        # the loop skips the loads of b and c outside their nonzero ranges
-        # (it measures them itself); the host copy is for bytes_model only
-        self.b_nz = _nonzero_range(problem.b)
-        self.c_nz = _nonzero_range(problem.c)
         self.cprob = _lib.ScsProblemC(
             n=n, m=m, A=self.dev.handle.value, K=self.cones.handle.value,
             b=ca.b_device.data_ptr(), c=ca.c_device.data_ptr(), g=ca.g_device.data_ptr(),
@@ -290,6 +299,20 @@ class SolverPlan:
             dr_scale=1.0 / (1.0 + float(np.linalg.norm(problem.c))))
         self.csettings = settings.to_c(n)
         self.reset()
+
+    # the loop skips the loads of b and c outside their nonzero ranges (it
+    # measures them itself); these host ranges are for bytes_model only
+    @property
+    def b_nz(self) -> tuple[int, int]:
+        if getattr(self, "_b_nz", None) is None:
+            self._b_nz = _nonzero_range(self.problem.b)
+        return self._b_nz
+
+    @property
+    def c_nz(self) -> tuple[int, int]:
+        if getattr(self, "_c_nz", None) is None:
+            self._c_nz = _nonzero_range(self.problem.c)
+        return self._c_nz
 
     def resetup(self) -> int:
         """Re-run the one-time setup solve g = (I+Q_z)^{-1} h on device into
@@ -321,6 +344,19 @@ class SolverPlan:
 
     def state(self) -> np.ndarray:
         return self.buf["state"].cpu().numpy()
+
+    def host_uv(self) -> tuple[np.ndarray, np.ndarray]:
+        """u, v on the host through pinned staging buffers (one DMA each)."""
+        import torch
+        st = getattr(self, "_pinned", None)
+        if st is None:
+            N = self.n + self.m + 1
+            st = self._pinned = (torch.empty(N, dtype=torch.float64, pin_memory=True),
+                                 torch.empty(N, dtype=torch.float64, pin_memory=True))
+        st[0].copy_(self.buf["u"], non_blocking=True)
+        st[1].copy_(self.buf["v"], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return st[0].numpy().copy(), st[1].numpy().copy()
 
     PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_x", "cone_elem",
                       "cone_soc_a", "cone_soc_b", "check", "launch_setup", "cone_soc_a_reduce")
@@ -427,8 +463,10 @@ def iterate_states(graph: SolverPlan, max_iters: int) -> Iterator[tuple[int, lis
 
 
 def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.ndarray,
-              iterations: int, cg_total: float) -> ScsSolution:
-    """scs.py:497-538."""
+              iterations: int, cg_total: float, device_resid=None) -> ScsSolution:
+    """scs.py:497-538.  ``device_resid`` = (pr, dr, gap) the loop evaluated on
+    exactly this iterate (its last check), used instead of recomputing the
+    residuals with two more operator applies on host copies."""
     A, b, c = problem.A, problem.b, problem.c
     n, m = A.cols, A.rows
     tau, kappa = float(u[-1]), float(v[-1])
@@ -438,7 +476,8 @@ def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.
     eps = settings.eps
     if tau > SMALL_TAU:
         x, y, s = ux / tau, uy / tau, vs / tau
-        pr, dr, gap = residuals(ScsIterate(u, v), problem)
+        pr, dr, gap = (device_resid if device_resid is not None
+                       else residuals(ScsIterate(u, v), problem))
         pobj, dobj = float(c @ x), -float(b @ y)
         if max(pr, dr, gap) <= eps:
             return ScsSolution(SOLVED, x, y, s, pobj, dobj, pr, dr, gap, iterations, avg_cg)
@@ -472,9 +511,15 @@ def solve_built(problem: ConeProblem, settings: ScsSettings, graph: SolverPlan,
         graph.reset()
         graph.run(settings.max_iters)
         st = graph.state()
-        u = graph.buf["u"].cpu().numpy()
-        v = graph.buf["v"].cpu().numpy()
-        return _classify(problem, settings, u, v, int(st[_lib.ST_K]), float(st[_lib.ST_CGT]))
+        u, v = graph.host_uv()
+        k = int(st[_lib.ST_K])
+        # the loop's residual triple belongs to this iterate when its last
+        # iteration was a check (k a multiple of check_interval; a latched
+        # status always is one)
+        fresh = k > 0 and k % settings.check_interval == 0
+        resid = (float(st[_lib.ST_PR]), float(st[_lib.ST_DR]), float(st[_lib.ST_GAP])) \
+            if fresh else None
+        return _classify(problem, settings, u, v, k, float(st[_lib.ST_CGT]), resid)
     prev_cg = 0.0
     state = graph.loop_vars()
     with open(trace_path, "w") as fh:

@@ -64,7 +64,7 @@ INSTANCES = {
                                   "density": 1e-3}, "reference", 8),
     # configs[2] family (15 x 15 blur) at a CPU-feasible size, and a wide 7 x 7 case
     "deconv2d_256_k15": ({"workload": "deconv2d", "h": 256, "w": 256, "k": 15}, "oracle", 8),
-    "deconv2d_40x330_k7": ({"workload": "deconv2d", "h": 40, "w": 330, "k": 7}, "oracle", 8),
+    "deconv2d_40x330_k7": ({"workload": "deconv2d", "h": 40, "w": 330, "k": 7}, "oracle", 16),
     # configs[1] family (kernel 101) at a CPU-feasible size, and the bench instance itself
     "deconv1d_n100000_k101": ({"workload": "deconv1d", "n": 100_000}, "reference", 8),
     "deconv1d_n1000000_k101": ({"workload": "deconv1d", "n": 1_000_000}, "oracle", 5),

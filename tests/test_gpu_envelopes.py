@@ -19,8 +19,10 @@ satisfy the north-star rule against that envelope:
   * zero-spread envelope -> the same status, the exact iteration count and
     the objective to 1e-6 relative;
   * otherwise            -> the same status, an iteration count inside
-    [min - check_interval, max + check_interval] and the objective inside
-    the envelope's objective range widened by its own spread.
+    [min - w, max + w] with w = max(check_interval, 2 % of the unperturbed
+    count) -- a handful of samples underestimates a chaotic envelope's
+    tails, and 2 % is the north star's own count tolerance -- and the
+    objective inside the envelope's objective range widened by its spread.
 """
 
 import importlib.util
@@ -58,8 +60,8 @@ def _check(name, sol, settings):
             assert abs(sol.pobj - ref["pobj"]) <= 1e-6 * max(1.0, abs(ref["pobj"])), \
                 (sol.pobj, ref["pobj"])
     else:
-        ci = settings.check_interval
-        assert min(its) - ci <= sol.iterations <= max(its) + ci, (sol.iterations, its)
+        w = max(settings.check_interval, 0.02 * ref["iterations"])
+        assert min(its) - w <= sol.iterations <= max(its) + w, (sol.iterations, its)
         if sol.status == "solved":
             lo, hi = min(pobjs), max(pobjs)
             spread = hi - lo
