@@ -32,7 +32,7 @@ def up_to_date() -> bool:
 
 
 # translation units compiled in parallel (see the CGB_TU_* flags in cgb200.cu)
-UNITS = ["CGB_TU_HOST", "CGB_TU_SCS0", "CGB_TU_SCS1", "CGB_TU_CG", "CGB_TU_INNER",
+UNITS = ["CGB_TU_HOST", "CGB_TU_SCS0", "CGB_TU_SCS1", "CGB_TU_SCS2", "CGB_TU_CG", "CGB_TU_INNER",
          "CGB_TU_MISC", "CGB_TU_SHARD"]
 
 

@@ -40,6 +40,7 @@
 #define CGB_TU_INNER 1
 #define CGB_TU_MISC 1
 #define CGB_TU_SHARD 1
+#define CGB_TU_SCS2 1
 #endif
 #ifndef CGB_TU_HOST
 #define CGB_TU_HOST 0
@@ -61,6 +62,9 @@
 #endif
 #ifndef CGB_TU_SHARD
 #define CGB_TU_SHARD 0
+#endif
+#ifndef CGB_TU_SCS2
+#define CGB_TU_SCS2 0
 #endif
 
 using namespace cgb;
@@ -448,7 +452,7 @@ struct CgUpdDirect {
 // Runs CG from r = b - apply(x) (stored in B.r) with rns = r.r.  Returns the
 // iteration count.  With tracking (B.c != null) *cx += alpha c.p and
 // *bax += alpha b.t follow c.x and b.(A x) through the updates.
-template <bool TD>
+template <int TD>
 __device__ int64_t cg_loop(const DevPlan& F, const DevPlan& Aj, int recipe, double lam,
                            const CgBufs& B, int64_t n, int64_t m, double& rns, double delta,
                            double floor_, int64_t max_iter, GridSync& gs, double* cx,
@@ -541,7 +545,7 @@ struct ApplyArgs {
   const double* x; double* y;
 };
 
-template <bool TD>
+template <int TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_apply(const __grid_constant__ ApplyArgs a) 
 #if CGB_TU_MISC
 {
@@ -601,7 +605,7 @@ struct CgArgs {
   double* result;  // [iterations, rns, bnorm2]
 };
 
-template <bool TD>
+template <int TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_cg(const __grid_constant__ CgArgs a) 
 #if CGB_TU_CG
 {
@@ -667,7 +671,7 @@ __device__ __forceinline__ double side_dot(int64_t n, const double* x, const dou
 
 // Inner block solve, the reference's arithmetic (scs.py:170-187):
 // rhs = d1 - A^T d2 ; r0 = rhs - (x0 + A^T A x0) ; CG ; z2 = d2 + A z1.
-template <bool TD>
+template <int TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_inner(const __grid_constant__ InnerArgs a) 
 #if CGB_TU_INNER
 {
@@ -897,9 +901,9 @@ struct SocPassB2 {
   }
 };
 
-template <bool TD>
+template <int TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_constant__ ScsArgs a) 
-#if CGB_TU_SCS0 || CGB_TU_SCS1
+#if CGB_TU_SCS0 || CGB_TU_SCS1 || CGB_TU_SCS2
 {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
   tma_init();
@@ -1251,25 +1255,28 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_barrier(const __grid_co
 
 // explicit instantiations, one group per translation unit
 #if CGB_TU_SCS0
-template __global__ void k_scs<false>(const __grid_constant__ ScsArgs);
+template __global__ void k_scs<0>(const __grid_constant__ ScsArgs);
 #endif
 #if CGB_TU_SCS1
-template __global__ void k_scs<true>(const __grid_constant__ ScsArgs);
+template __global__ void k_scs<1>(const __grid_constant__ ScsArgs);
+#endif
+#if CGB_TU_SCS2
+template __global__ void k_scs<2>(const __grid_constant__ ScsArgs);
 #endif
 #if CGB_TU_CG
-template __global__ void k_cg<false>(const __grid_constant__ CgArgs);
-template __global__ void k_cg<true>(const __grid_constant__ CgArgs);
+template __global__ void k_cg<0>(const __grid_constant__ CgArgs);
+template __global__ void k_cg<1>(const __grid_constant__ CgArgs);
 #endif
 #if CGB_TU_INNER
-template __global__ void k_inner<false>(const __grid_constant__ InnerArgs);
-template __global__ void k_inner<true>(const __grid_constant__ InnerArgs);
+template __global__ void k_inner<0>(const __grid_constant__ InnerArgs);
+template __global__ void k_inner<1>(const __grid_constant__ InnerArgs);
 #endif
 #if CGB_TU_SHARD
-template __global__ void k_shard<false>(const __grid_constant__ ShardArgs);
+template __global__ void k_shard<0>(const __grid_constant__ ShardArgs);
 #endif
 #if CGB_TU_MISC
-template __global__ void k_apply<false>(const __grid_constant__ ApplyArgs);
-template __global__ void k_apply<true>(const __grid_constant__ ApplyArgs);
+template __global__ void k_apply<0>(const __grid_constant__ ApplyArgs);
+template __global__ void k_apply<1>(const __grid_constant__ ApplyArgs);
 #endif
 
 }  // namespace cgbk
@@ -1322,6 +1329,7 @@ struct PlanStore {
   int64_t temp_total = 0;
   int64_t in_len = 0, out_len = 0;
   int64_t leaf_bytes = 0;   // operand bytes of one apply (cluster-mode choice)
+  bool has_dense = false;   // a dense leaf: the solver runs its MODE 2 instantiation
 };
 
 struct cgb_op {
@@ -1818,8 +1826,10 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   ps->in_len = d->in_len;
   ps->out_len = d->out_len;
   ps->leaf_bytes = 0;
+  ps->has_dense = false;
   for (const cgb_leaf& L : leaves) {
     if (L.kind == CGB_LEAF_DENSE) ps->leaf_bytes += 8 * L.rows * L.cols;
+    if (L.kind == CGB_LEAF_DENSE) ps->has_dense = true;
     if (L.kind == CGB_LEAF_CSR) {
       int64_t nnz = 0;
       CUDA_TRY(cudaMemcpy(&nnz, L.rowptr + L.rows, sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -1900,7 +1910,7 @@ int cgb_ctx_destroy(cgb_ctx* ctx) {
 int cgb_ctx_geometry(const cgb_ctx* ctx, int32_t* out3) {
   if (!ctx || !out3) return fail(CGB_EINVAL, "null argument");
   int grid = 0;
-  int rc = grid_for(ctx, k_scs<false>, 0, &grid);
+  int rc = grid_for(ctx, k_scs<0>, 0, &grid);
   if (rc) return rc;
   out3[0] = ctx->num_sms;
   out3[1] = grid / ctx->num_sms;
@@ -1942,8 +1952,8 @@ int cgb_op_apply(cgb_ctx* ctx, const cgb_op* op, int adjoint, const double* x, d
   if (op->ctx != ctx) return fail(CGB_EINVAL, "operator belongs to another ctx");
   std::lock_guard<std::mutex> lk(ctx->mu);
   ApplyArgs a{ctx->bar, ctx->partials, adjoint ? op->adj.dp : op->fwd.dp, x, y};
-  if (a.P.smem_xs2 > 0) return launch_coop(ctx, k_apply<true>, a, plan_smem(a.P), (cudaStream_t)stream);
-  return launch_coop(ctx, k_apply<false>, a, plan_smem(a.P), (cudaStream_t)stream);
+  if (a.P.smem_xs2 > 0) return launch_coop(ctx, k_apply<1>, a, plan_smem(a.P), (cudaStream_t)stream);
+  return launch_coop(ctx, k_apply<0>, a, plan_smem(a.P), (cudaStream_t)stream);
 }
 
 int cgb_cones_create(cgb_ctx* ctx, const int32_t* kinds, const int64_t* dims, int32_t ncones,
@@ -2047,8 +2057,8 @@ int cgb_cg_solve(cgb_ctx* ctx, const cgb_op* op, int recipe, double lam, const d
            scratch, scratch + n, scratch + 2 * n, scratch + 3 * n,
            n, m, tol, max_iter, eps_floor_for(n), ctx->result};
   int rc = (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
-               ? launch_coop(ctx, k_cg<true>, a, solver_smem(a.F, a.Aj), s)
-               : launch_coop(ctx, k_cg<false>, a, solver_smem(a.F, a.Aj), s);
+               ? launch_coop(ctx, k_cg<1>, a, solver_smem(a.F, a.Aj), s)
+               : launch_coop(ctx, k_cg<0>, a, solver_smem(a.F, a.Aj), s);
   cudaError_t ce = cudaSuccess;
   if (rc == CGB_OK)
     ce = cudaMemcpyAsync(ctx->host_result, ctx->result, 3 * sizeof(double),
@@ -2081,8 +2091,8 @@ int cgb_inner_solve(cgb_ctx* ctx, const cgb_op* op, const double* d1, const doub
               n, m, tol, max_iter, eps_floor_for(n), ctx->result};
   const int cs = cluster_size_for(n, m, op->fwd.leaf_bytes + op->adj.leaf_bytes);
   int rc = (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
-               ? launch_coop(ctx, k_inner<true>, a, solver_smem(a.F, a.Aj), s, cs)
-               : launch_coop(ctx, k_inner<false>, a, solver_smem(a.F, a.Aj), s, cs);
+               ? launch_coop(ctx, k_inner<1>, a, solver_smem(a.F, a.Aj), s, cs)
+               : launch_coop(ctx, k_inner<0>, a, solver_smem(a.F, a.Aj), s, cs);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(ctx->host_result, ctx->result, 4 * sizeof(double),
                            cudaMemcpyDeviceToHost, s));
@@ -2158,8 +2168,10 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.stash_cap = (int)(smem / sizeof(double));
   const int cs = cluster_size_for(prob->n, prob->m, op->fwd.leaf_bytes + op->adj.leaf_bytes);
   if (a.F.smem_xs2 > 0 || a.Aj.smem_xs2 > 0)
-    return launch_coop(ctx, k_scs<true>, a, smem, (cudaStream_t)stream, cs);
-  return launch_coop(ctx, k_scs<false>, a, smem, (cudaStream_t)stream, cs);
+    return launch_coop(ctx, k_scs<1>, a, smem, (cudaStream_t)stream, cs);
+  if (op->fwd.has_dense || op->adj.has_dense)
+    return launch_coop(ctx, k_scs<2>, a, smem, (cudaStream_t)stream, cs);
+  return launch_coop(ctx, k_scs<0>, a, smem, (cudaStream_t)stream, cs);
 }
 
 int cgb_ctx_set_grid(cgb_ctx* ctx, int32_t grid) {
@@ -2293,7 +2305,7 @@ int cgb_shard_run(cgb_ctx* ctx, const cgb_shard_problem* prob, const cgb_scs_set
   a.setup_tol = prob->setup_tol;
   a.max_steps = max_steps;
   a.mode = mode;
-  return launch_coop(ctx, k_shard<false>, a, solver_smem(a.F, a.Aj), (cudaStream_t)stream);
+  return launch_coop(ctx, k_shard<0>, a, solver_smem(a.F, a.Aj), (cudaStream_t)stream);
 }
 
 int cgb_ipc_alloc(int device, int64_t bytes, void** ptr, void* handle64) {

@@ -682,6 +682,93 @@ static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0
   tile_transpose(y, os, acc, alpha, nvalid, lane);
 }
 
+// Dense rows of a tile: a warp per row, CGB_DENSE_DR rows at a time so
+// their loads are in flight together (one latency per row group instead of
+// per row).  Two copies: dense_rows (inlined) and dense_tile (out of line,
+// its own register allocation).  Inlined into the persistent solver kernel
+// the loop ran at a third of its stand-alone bandwidth (2.0 vs 6.0 TB/s on
+// configs[4]'s 2e5 x 2e3 operator); the host launches the MODE 2
+// instantiation -- which calls dense_tile -- for plans with dense leaves,
+// and the others keep the inline copy (the call site cost the convolution
+// plans ~8 % when always present).
+static __device__ __noinline__ void dense_tile(const cgb_leaf& L, int64_t lrow0, int nvalid,
+                                               InVec in, double alpha, double (&acc)[CGB_RC],
+                                               int lane) {
+  constexpr int CGB_DR = CGB_DENSE_DR;
+  constexpr int CGB_DU = CGB_DENSE_UNROLL;
+  double mine[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
+  const int64_t cols = L.cols;
+  for (int rr0 = 0; rr0 < nvalid; rr0 += CGB_DR) {
+    double sacc[CGB_DR];
+    const double* rowp[CGB_DR];
+#pragma unroll
+    for (int q = 0; q < CGB_DR; ++q) {
+      sacc[q] = 0.0;
+      const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
+      rowp[q] = L.val + (lrow0 + rr) * L.ld;
+    }
+#pragma unroll CGB_DU
+    for (int64_t c = lane; c < cols; c += 32) {
+      const double xv = in(c);
+#pragma unroll
+      for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+    }
+#pragma unroll
+    for (int q = 0; q < CGB_DR; ++q) {
+      const double sq = warp_sum(sacc[q]);
+      const int rr = rr0 + q;
+      if (rr < nvalid && lane == (rr & 31)) {
+#pragma unroll
+        for (int r = 0; r < CGB_RC; ++r)
+          if (r == (rr >> 5)) mine[r] = sq;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) acc[r] += alpha * mine[r];
+}
+
+__device__ __forceinline__ void dense_rows(const cgb_leaf& L, int64_t lrow0, int nvalid,
+                                               const InVec& in, double alpha, double (&acc)[CGB_RC],
+                                               int lane) {
+  constexpr int CGB_DR = CGB_DENSE_DR;
+  constexpr int CGB_DU = CGB_DENSE_UNROLL;
+  double mine[CGB_RC];
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
+  const int64_t cols = L.cols;
+  for (int rr0 = 0; rr0 < nvalid; rr0 += CGB_DR) {
+    double sacc[CGB_DR];
+    const double* rowp[CGB_DR];
+#pragma unroll
+    for (int q = 0; q < CGB_DR; ++q) {
+      sacc[q] = 0.0;
+      const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
+      rowp[q] = L.val + (lrow0 + rr) * L.ld;
+    }
+#pragma unroll CGB_DU
+    for (int64_t c = lane; c < cols; c += 32) {
+      const double xv = in(c);
+#pragma unroll
+      for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+    }
+#pragma unroll
+    for (int q = 0; q < CGB_DR; ++q) {
+      const double sq = warp_sum(sacc[q]);
+      const int rr = rr0 + q;
+      if (rr < nvalid && lane == (rr & 31)) {
+#pragma unroll
+        for (int r = 0; r < CGB_RC; ++r)
+          if (r == (rr >> 5)) mine[r] = sq;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < CGB_RC; ++r) acc[r] += alpha * mine[r];
+}
+
 // Contribution of one leaf to a warp tile.  The tile holds 32*R rows
 // starting at leaf-local row lrow0; lane l owns rows lrow0 + l + 32 r
 // (r < R), so epilogue stores are coalesced.  acc[r] accumulates.
@@ -690,7 +777,7 @@ static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0
 // 1-d convolution / correlation leaves in R == CGB_RC tiles run the
 // register-blocked path (conv_compute) on a window staged in shared memory:
 // by TMA in run_level for interior tiles, by hand (zero-filled edges) here.
-template <bool WITH2D>
+template <int MODE>
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
                                           double (&acc)[CGB_RC], int lane, const double* cc,
@@ -707,44 +794,13 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
       for (int r = 0; r < CGB_RC; ++r)
         if (r < R && lane + 32 * r < nvalid) acc[r] += alpha * v[r];
     } break;
-    case CGB_LEAF_DENSE: {
-      // warp per row, CGB_DR rows at a time so their loads are in flight
-      // together (one latency per row group instead of per row)
-      constexpr int CGB_DR = CGB_DENSE_DR;
-      constexpr int CGB_DU = CGB_DENSE_UNROLL;
-      double mine[CGB_RC];
-#pragma unroll
-      for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
-      const int64_t cols = L.cols;
-      for (int rr0 = 0; rr0 < nvalid; rr0 += CGB_DR) {
-        double sacc[CGB_DR];
-        const double* rowp[CGB_DR];
-#pragma unroll
-        for (int q = 0; q < CGB_DR; ++q) {
-          sacc[q] = 0.0;
-          const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
-          rowp[q] = L.val + (lrow0 + rr) * L.ld;
-        }
-#pragma unroll CGB_DU
-        for (int64_t c = lane; c < cols; c += 32) {
-          const double xv = in(c);
-#pragma unroll
-          for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
-        }
-#pragma unroll
-        for (int q = 0; q < CGB_DR; ++q) {
-          const double sq = warp_sum(sacc[q]);
-          const int rr = rr0 + q;
-          if (rr < nvalid && lane == (rr & 31)) {
-#pragma unroll
-            for (int r = 0; r < CGB_RC; ++r)
-              if (r == (rr >> 5)) mine[r] = sq;
-          }
-        }
+    case CGB_LEAF_DENSE:
+      if (MODE == 2) {
+        dense_tile(L, lrow0, nvalid, in, alpha, acc, lane);
+      } else {
+        dense_rows(L, lrow0, nvalid, in, alpha, acc, lane);
       }
-#pragma unroll
-      for (int r = 0; r < CGB_RC; ++r) acc[r] += alpha * mine[r];
-    } break;
+      break;
     case CGB_LEAF_CSR: {
 #pragma unroll
       for (int r = 0; r < CGB_RC; ++r) {
@@ -818,10 +874,10 @@ __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int 
     } break;
     case CGB_LEAF_CONV2D:
     case CGB_LEAF_CORR2D: {
-      // the tiled 2-d path (a call) exists only in the WITH2D kernels, which
+      // the tiled 2-d path (a call) exists only in the MODE 1 kernels, which
       // the host launches for plans with a 2-d leaf: it cost every other
       // plan ~10 % (register allocation around the call) when always present
-      if (WITH2D && R == CGB_RC && cc && ring) {
+      if (MODE == 1 && R == CGB_RC && cc && ring) {
         conv2d_tile(L, lrow0, nvalid, in.a, alpha, cc, ring, xs2, os, acc, lane);
         break;
       }
@@ -934,7 +990,7 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
       : "memory");
 }
 
-template <bool WITH2D>
+template <int MODE>
 __device__ __forceinline__ void leaf_tile(const cgb_leaf& L, int64_t lrow0, int nvalid, int R,
                                           const InVec& in, double alpha,
                                           double (&acc)[CGB_RC], int lane, const double* cc,
@@ -1104,11 +1160,11 @@ static __device__ __noinline__ void strip_rowpass(int64_t kw, const double* t, c
 // run per warp on its output row segment, exactly as in run_level.
 // Returns false (nothing done) when the apply input is a fused two-vector
 // accessor, which the strips do not stage.
-template <bool WITH2D, class Epi>
+template <int MODE, class Epi>
 __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
                            double* part) {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
-  if (!WITH2D || P.strip_rows == 0) return false;
+  if (MODE != 1 || P.strip_rows == 0) return false;
   if (in.b) return false;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int rb_lo = P.level_rb[e], rb_hi = P.level_rb[e + 1];
@@ -1279,7 +1335,7 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
                                   ? in.shift(tt.in_off)
                                   : InVec{temp + P.temp_off[tt.in_buf - 1] + tt.in_off, nullptr,
                                           0.0};
-            leaf_tile<false>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
+            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
                              nullptr, nullptr, os, nullptr, 0);
           }
           if (rb.out_buf == 0) {
@@ -1313,11 +1369,11 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
 // epi.tile(first_row, tile_row0, R, left, acc, part) with rows first_row + 32 r,
 // valid while 32 r < left (see CGB_EPI_VALID) -- so it can issue all its
 // loads before its stores.
-template <bool WITH2D, class Epi>
+template <int MODE, class Epi>
 __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi& epi,
                           double* part) {
   extern __shared__ __align__(16) double cgb_dyn_smem[];
-  const bool strips = run_strips<WITH2D>(P, e, in, ts, epi, part);
+  const bool strips = run_strips<MODE>(P, e, in, ts, epi, part);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* xsb0 = cgb_dyn_smem + (size_t)wib * P.smem_per_warp;
   double* xsb1 = xsb0 + P.smem_xs;
@@ -1340,7 +1396,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
   if (tile < T) {
     rbi = find_rowblock(P, rb_lo, rb_hi, tile);
     const DevRowBlock& rb = P.rbs[rbi];
-    tile_rows<WITH2D>(rb, tile, row0, nvalid);
+    tile_rows<MODE == 1>(rb, tile, row0, nvalid);
     win = conv_window(P, rb, row0, in, temp);
     if (win.ok) issue_window(win, xsb0, &bar[0], lane);
   }
@@ -1359,7 +1415,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
     if (ntile < T) {
       nrbi = find_rowblock(P, rb_lo, rb_hi, ntile);
       const DevRowBlock& nrb = P.rbs[nrbi];
-      tile_rows<WITH2D>(nrb, ntile, nrow0, nnvalid);
+      tile_rows<MODE == 1>(nrb, ntile, nrow0, nnvalid);
       nwin = conv_window(P, nrb, nrow0, in, temp);
       if (nwin.ok) issue_window(nwin, cur ? xsb0 : xsb1, &bar[cur ^ 1], lane);
     }
@@ -1393,7 +1449,7 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
       const InVec tin = tm.in_buf == 0
                             ? in.shift(tm.in_off)
                             : InVec{temp + P.temp_off[tm.in_buf - 1] + tm.in_off, nullptr, 0.0};
-      leaf_tile<WITH2D>(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os,
+      leaf_tile<MODE>(L, row0 - tm.row_origin, nvalid, R, tin, tm.alpha, acc, lane, cc, xcur, os,
                 tin.b ? nullptr : ring, P.smem_xs2);
     }
     if (tl) { const uint64_t x = globaltimer(); tl[3] += (double)(x - tl1); tl1 = x; }
@@ -1425,27 +1481,27 @@ __device__ void run_level(const DevPlan& P, int e, const InVec& in, int ts, Epi&
 
 // Full application; levels separated by grid barriers.  No barrier after the
 // final level: the caller follows with a reduction or sync.
-template <bool WITH2D, class Epi>
+template <int MODE, class Epi>
 __device__ void apply_plan(const DevPlan& P, const InVec& in, Epi& epi, double* part,
                            GridSync& gs, int ts = 0) {
   for (int e = 0; e < P.nlevels; ++e) {
     if (e) gs.sync();
-    run_level<WITH2D>(P, e, in, ts, epi, part);
+    run_level<MODE>(P, e, in, ts, epi, part);
   }
 }
 
 // Two independent applications in one phase (levels aligned at the end);
 // the second uses temporary set 1, so both may be the same plan.
-template <bool WITH2D, class E1, class E2>
+template <int MODE, class E1, class E2>
 __device__ void apply_two(const DevPlan& P1, const InVec& in1, E1& e1, const DevPlan& P2,
                           const InVec& in2, E2& e2, double* part, GridSync& gs) {
   const int L = P1.nlevels > P2.nlevels ? P1.nlevels : P2.nlevels;
   for (int s = 0; s < L; ++s) {
     if (s) gs.sync();
     const int a = s - (L - P1.nlevels);
-    if (a >= 0) run_level<WITH2D>(P1, a, in1, 0, e1, part);
+    if (a >= 0) run_level<MODE>(P1, a, in1, 0, e1, part);
     const int b = s - (L - P2.nlevels);
-    if (b >= 0) run_level<WITH2D>(P2, b, in2, 1, e2, part);
+    if (b >= 0) run_level<MODE>(P2, b, in2, 1, e2, part);
   }
 }
 

@@ -28,7 +28,7 @@ struct ShardArgs {
 // CG on (I + A^T A) x = rhs from r (= xfull[x0:x0+nl]) with rns = r.r;
 // the k_scs cg_loop (normal recipe, lam = 1) with world reductions.
 // track: cx += alpha c.p and bax += alpha b.t follow c.x and b.(A x).
-template <bool TD>
+template <int TD>
 __device__ int64_t cg_shard(const DevPlan& F, const DevPlan& Aj, const ShardArgs& a,
                             double* x, double* gx, double* ax, bool track, double& rns,
                             double delta, double floor_, int64_t max_iter, GridSync& gs,
@@ -108,7 +108,7 @@ __device__ int64_t cg_shard(const DevPlan& F, const DevPlan& Aj, const ShardArgs
   return k;
 }
 
-template <bool TD>
+template <int TD>
 __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_shard(const __grid_constant__ ShardArgs a)
 #if CGB_TU_SHARD
 {

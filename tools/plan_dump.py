@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_1609_03488_b200 import _lib, scs  # noqa: E402
 
-KIND = {v: k for k, v in vars(_lib).items() if k.startswith("LEAF_")}
+KIND = {v: k for k, v in vars(_lib).items() if k.startswith("LEAF_") and not k.startswith("LEAF_FLAG")}
 
 
 class A:
