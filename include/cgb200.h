@@ -207,6 +207,8 @@ typedef struct cgb_scs_work {
 #define CGB_ST_DENOM 10    /* shard solver: 1 + h.g of the setup solve          */
 #define CGB_ST_EPOCH 11    /* shard solver: world synchronisations so far       */
 #define CGB_ST_SETUP_CG 12 /* shard solver: CG iterations of the setup solve    */
+#define CGB_ST_RES_U 13    /* last check: unboundedness certificate residual   */
+#define CGB_ST_RES_I 14    /* last check: infeasibility certificate residual   */
 #define CGB_STATE_LEN 16
 
 #define CGB_SCS_NO_ZERO_SKIP 1  /* cgb_scs_problem.flags: stream all of b and c */

@@ -27,7 +27,7 @@ CONE_ZERO, CONE_NONNEG, CONE_SOC, CONE_EXP = range(4)
 RECIPE_DIRECT, RECIPE_NORMAL = 0, 1
 
 ST_K, ST_SINCE, ST_STATUS, ST_CGT, ST_PR, ST_DR, ST_GAP, ST_LASTCG = range(8)
-ST_TAU, ST_KAPPA, ST_DENOM, ST_EPOCH, ST_SETUP_CG = range(8, 13)
+ST_TAU, ST_KAPPA, ST_DENOM, ST_EPOCH, ST_SETUP_CG, ST_RES_U, ST_RES_I = range(8, 15)
 MAX_RANKS = 8
 MBOX_STRIDE = 24
 STATE_LEN = 16

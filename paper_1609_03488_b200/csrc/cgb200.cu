@@ -918,6 +918,7 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
   double k = state[CGB_ST_K], since = state[CGB_ST_SINCE], status = state[CGB_ST_STATUS];
   double cgt = state[CGB_ST_CGT];
   double pr = state[CGB_ST_PR], dr = state[CGB_ST_DR], gap = state[CGB_ST_GAP];
+  double res_u_last = state[CGB_ST_RES_U], res_i_last = state[CGB_ST_RES_I];
   double lastcg = state[CGB_ST_LASTCG];
   const int64_t cg_max = S.cg_max_iter;
   int64_t steps = 0;
@@ -1182,10 +1183,12 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
       const double den_u = fmax(-1.0 * ctx, 0.0);
       const double pos_u = den_u > 0.0 ? 1.0 : 0.0;
       const double res_u = sqrt(q[1]) / (den_u + (1.0 - pos_u));
+      res_u_last = res_u;
       const double unb_ok = pos_u * (eps > res_u ? 1.0 : 0.0);
       const double den_i = fmax(-1.0 * bty, 0.0);
       const double pos_i = den_i > 0.0 ? 1.0 : 0.0;
       const double res_i = sqrt(q[3]) / (den_i + (1.0 - pos_i));
+      res_i_last = res_i;
       const double inf_ok = pos_i * (eps > res_i ? 1.0 : 0.0);
       const double cert = tau_small * (2.0 * inf_ok + (1.0 - inf_ok) * (3.0 * unb_ok));
       const double cand = solved + (1.0 - solved) * cert;
@@ -1206,6 +1209,8 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     state[CGB_ST_DR] = dr;
     state[CGB_ST_GAP] = gap;
     state[CGB_ST_LASTCG] = lastcg;
+    state[CGB_ST_RES_U] = res_u_last;
+    state[CGB_ST_RES_I] = res_i_last;
   }
 }
 #else

@@ -346,17 +346,17 @@ class SolverPlan:
         return self.buf["state"].cpu().numpy()
 
     def host_uv(self) -> tuple[np.ndarray, np.ndarray]:
-        """u, v on the host through pinned staging buffers (one DMA each)."""
+        """u, v on the host: one DMA each into page-locked buffers from
+        torch's caching host allocator, handed out as numpy views (the
+        buffers live as long as the arrays)."""
         import torch
-        st = getattr(self, "_pinned", None)
-        if st is None:
-            N = self.n + self.m + 1
-            st = self._pinned = (torch.empty(N, dtype=torch.float64, pin_memory=True),
-                                 torch.empty(N, dtype=torch.float64, pin_memory=True))
-        st[0].copy_(self.buf["u"], non_blocking=True)
-        st[1].copy_(self.buf["v"], non_blocking=True)
+        N = self.n + self.m + 1
+        hu = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        hv = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        hu.copy_(self.buf["u"], non_blocking=True)
+        hv.copy_(self.buf["v"], non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return st[0].numpy().copy(), st[1].numpy().copy()
+        return hu.numpy(), hv.numpy()
 
     PROFILE_PHASES = ("rhs", "cg_forward", "cg_adjoint_update", "cone_x", "cone_elem",
                       "cone_soc_a", "cone_soc_b", "check", "launch_setup", "cone_soc_a_reduce")
@@ -464,9 +464,10 @@ def iterate_states(graph: SolverPlan, max_iters: int) -> Iterator[tuple[int, lis
 
 def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.ndarray,
               iterations: int, cg_total: float, device_resid=None) -> ScsSolution:
-    """scs.py:497-538.  ``device_resid`` = (pr, dr, gap) the loop evaluated on
-    exactly this iterate (its last check), used instead of recomputing the
-    residuals with two more operator applies on host copies."""
+    """scs.py:497-538.  ``device_resid`` = (pr, dr, gap, res_u, res_i) the
+    loop evaluated on exactly this iterate (its last check), used instead
+    of recomputing the residuals / certificate residuals with operator
+    applies on host copies."""
     A, b, c = problem.A, problem.b, problem.c
     n, m = A.cols, A.rows
     tau, kappa = float(u[-1]), float(v[-1])
@@ -476,7 +477,7 @@ def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.
     eps = settings.eps
     if tau > SMALL_TAU:
         x, y, s = ux / tau, uy / tau, vs / tau
-        pr, dr, gap = (device_resid if device_resid is not None
+        pr, dr, gap = (device_resid[:3] if device_resid is not None
                        else residuals(ScsIterate(u, v), problem))
         pobj, dobj = float(c @ x), -float(b @ y)
         if max(pr, dr, gap) <= eps:
@@ -486,13 +487,15 @@ def _classify(problem: ConeProblem, settings: ScsSettings, u: np.ndarray, v: np.
         x = y = s = None
     den_i = -float(b @ uy)
     if den_i > 0:
-        res_i = float(np.linalg.norm(A.adjoint_apply(uy))) / den_i
+        res_i = (device_resid[4] if device_resid is not None
+                 else float(np.linalg.norm(A.adjoint_apply(uy))) / den_i)
         if tau < settings.cert_tau_ratio * max(kappa, 1.0) and res_i <= eps:
             return ScsSolution(INFEASIBLE, nan_n, uy / den_i, nan_m, np.nan, np.nan,
                                np.inf, res_i, np.inf, iterations, avg_cg)
     den_u = -float(c @ ux)
     if den_u > 0:
-        res_u = float(np.linalg.norm(A.forward(ux) + vs)) / den_u
+        res_u = (device_resid[3] if device_resid is not None
+                 else float(np.linalg.norm(A.forward(ux) + vs)) / den_u)
         if tau < settings.cert_tau_ratio * max(kappa, 1.0) and res_u <= eps:
             return ScsSolution(UNBOUNDED, ux / den_u, nan_m, vs / den_u, np.nan, np.nan,
                                res_u, np.inf, np.inf, iterations, avg_cg)
@@ -517,8 +520,8 @@ def solve_built(problem: ConeProblem, settings: ScsSettings, graph: SolverPlan,
         # iteration was a check (k a multiple of check_interval; a latched
         # status always is one)
         fresh = k > 0 and k % settings.check_interval == 0
-        resid = (float(st[_lib.ST_PR]), float(st[_lib.ST_DR]), float(st[_lib.ST_GAP])) \
-            if fresh else None
+        resid = (float(st[_lib.ST_PR]), float(st[_lib.ST_DR]), float(st[_lib.ST_GAP]),
+                 float(st[_lib.ST_RES_U]), float(st[_lib.ST_RES_I])) if fresh else None
         return _classify(problem, settings, u, v, k, float(st[_lib.ST_CGT]), resid)
     prev_cg = 0.0
     state = graph.loop_vars()

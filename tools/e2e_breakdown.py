@@ -43,7 +43,8 @@ for rep in range(2):
     u, v = g.host_uv()
     t["d2h_uv"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    resid = (float(stt[_lib.ST_PR]), float(stt[_lib.ST_DR]), float(stt[_lib.ST_GAP]))
+    resid = (float(stt[_lib.ST_PR]), float(stt[_lib.ST_DR]), float(stt[_lib.ST_GAP]),
+             float(stt[_lib.ST_RES_U]), float(stt[_lib.ST_RES_I]))
     sol = scs._classify(prob, st, u, v, int(stt[_lib.ST_K]), float(stt[_lib.ST_CGT]), resid)
     t["classify"] = time.perf_counter() - t0
     torch.cuda.synchronize()
