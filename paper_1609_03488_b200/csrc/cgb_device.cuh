@@ -1138,7 +1138,7 @@ static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t bas
 }
 
 // the row pass of a separable strip row: y = v * t (register-blocked)
-static __device__ __noinline__ void strip_rowpass(int64_t kw, const double* t, const double* taps,
+static __device__ __forceinline__ void strip_rowpass(int64_t kw, const double* t, const double* taps,
                                                   double (&yout)[CGB_RC], int lane) {
   double y[CGB_RC];
 #pragma unroll
@@ -1312,19 +1312,31 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
             a_lo = oi - (IH - 1) > 0 ? oi - (IH - 1) : 0;
             a_hi = oi < kh - 1 ? oi : kh - 1;
           }
+          // the tile of output row p, columns [oj0, oj0 + nvalid): every term
+          // in order.  The terms before the strip term are summed first, so
+          // their global loads are in flight during the row pass; then the
+          // strip term from y, then the rest -- the same order as a tile.
+          const int64_t row0 = rb.row_begin + p * OW + oj0;
+          double acc[CGB_RC];
+#pragma unroll
+          for (int r = 0; r < CGB_RC; ++r) acc[r] = 0.0;
+          for (int t = rb.term_begin; t < rb.strip_term; ++t) {
+            const cgb_term tt = P.terms[t];
+            const cgb_leaf LL = P.leaves[tt.leaf];
+            const InVec tin = tt.in_buf == 0
+                                  ? in.shift(tt.in_off)
+                                  : InVec{temp + P.temp_off[tt.in_buf - 1] + tt.in_off, nullptr,
+                                          0.0};
+            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
+                         nullptr, nullptr, os, nullptr, 0);
+          }
           double y[CGB_RC];
           if (sep)
             strip_rowpass(kw, tb, taps, y, lane);
           else
             strip_row(L, oi, a_lo, a_hi, tma ? x + clo : nullptr, IW, ring, SLOT, NS, taps, tb,
                       y, lane);
-          // the tile of output row p, columns [oj0, oj0 + nvalid): every term
-          // in order, the strip term from y
-          const int64_t row0 = rb.row_begin + p * OW + oj0;
-          double acc[CGB_RC];
-#pragma unroll
-          for (int r = 0; r < CGB_RC; ++r) acc[r] = 0.0;
-          for (int t = rb.term_begin; t < rb.term_end; ++t) {
+          for (int t = rb.strip_term; t < rb.term_end; ++t) {
             const cgb_term tt = P.terms[t];
             if (t == rb.strip_term) {
               tile_transpose(y, os, acc, tt.alpha, nvalid, lane);
