@@ -1468,6 +1468,14 @@ struct Blob {
   }
 };
 
+// doubles of dynamic shared memory of the 2-d strips for a kh-row kernel:
+// the row ring (kh + 2 RPS - 1 slots) and, per warp, the transpose buffer
+// and its t buffers (two when a warp has one row per step)
+int64_t strip_smem(int64_t kh, int64_t slot) {
+  const int64_t tb = CGB_STRIP_RPW == 1 ? 2 : CGB_STRIP_RPW;
+  return (kh + 2 * CGB_STRIP_RPS - 1) * slot + CGB_WARPS * (tb * slot + 32 * CGB_RC + 2);
+}
+
 int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   if (!d) return fail(CGB_EINVAL, "null plan descriptor");
   if (d->nleaves < 0 || d->nterms < 0 || d->nrowblocks < 1 || d->ntemps < 0)
@@ -1751,23 +1759,23 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
       const cgb_leaf& LF = leaves[d->terms[t2].leaf];
       const int64_t nt = (LF.k1 + CGB_RC - 1) / CGB_RC * CGB_RC;
       const int64_t slot = (32 * CGB_RC + nt + 2 + 1) & ~1;
-      const int64_t need = (LF.k0 + 15) * slot + CGB_WARPS * (2 * slot + 32 * CGB_RC + 2);
+      const int64_t need = strip_smem(LF.k0, slot);
       if (need > 24 * 1024) continue;  // 192 KB of shared memory at most
       D.strip_term = t2;
       khmax = std::max<int64_t>(khmax, LF.k0);
       ntmax = std::max<int64_t>(ntmax, nt);
     }
     const int64_t slot_all = (32 * CGB_RC + ntmax + 2 + 1) & ~1;
-    if (khmax > 0 &&
-        (khmax + 15) * slot_all + CGB_WARPS * (2 * slot_all + 32 * CGB_RC + 2) > 24 * 1024) {
+    if (khmax > 0 && strip_smem(khmax, slot_all) > 24 * 1024) {
       for (DevRowBlock& D : rbs) D.strip_term = -1;   // several kernels: over budget together
       khmax = 0;
     }
     if (khmax > 0) {
       strip_slot = (int32_t)((32 * CGB_RC + ntmax + 2 + 1) & ~1);
-      strip_nslot = (int32_t)(khmax + 15);
-      int rows = 32;
-      if (const char* er = std::getenv("CGB_STRIP_ROWS")) rows = std::max(8, std::atoi(er) / 8 * 8);
+      strip_nslot = (int32_t)(khmax + 2 * CGB_STRIP_RPS - 1);
+      int rows = 4 * CGB_STRIP_RPS;
+      if (const char* er = std::getenv("CGB_STRIP_ROWS"))
+        rows = std::max(CGB_STRIP_RPS, std::atoi(er) / CGB_STRIP_RPS * CGB_STRIP_RPS);
       strip_rows = rows;
     }
   }
@@ -1824,8 +1832,7 @@ int build_plan(const cgb_plan_desc* d, PlanStore* ps) {
   P.smem_total = CGB_WARPS * P.smem_per_warp;
   if (P.strip_rows > 0)
     P.smem_total = std::max<int32_t>(
-        P.smem_total,
-        P.strip_nslot * P.strip_slot + CGB_WARPS * (2 * P.strip_slot + 32 * CGB_RC + 2));
+        P.smem_total, (int32_t)strip_smem(P.strip_nslot - 2 * CGB_STRIP_RPS + 1, P.strip_slot));
   P.in_len = d->in_len;
   P.out_len = d->out_len;
   ps->in_len = d->in_len;

@@ -38,6 +38,10 @@
 #endif
 #define CGB_CONV_KMAX 240    // longest 1-d kernel of the register-blocked (TMA) tile path
 #define CGB_SEP_KMAX 63      // widest rank-one 2-d kernel applied as column + row passes
+#ifndef CGB_STRIP_RPW
+#define CGB_STRIP_RPW 1      // output rows per warp per strip step
+#endif
+#define CGB_STRIP_RPS (CGB_WARPS * CGB_STRIP_RPW)  // output rows per strip step
 #ifndef CGB_U
 #define CGB_U 8              // elements per thread per batch in streaming loops
 #endif
@@ -1082,9 +1086,10 @@ static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t bas
   // shared-memory offset of every row the step reads (kh + 7 of them, at
   // most CGB_SEP_KMAX + 7), -1 for rows outside the image: computed once,
   // so the column loop's loads are one add + one shared load each
-  constexpr int kMaxRows = 64 + CGB_WARPS;
+  constexpr int RPS = CGB_STRIP_RPS;
+  constexpr int kMaxRows = 64 + RPS;
   __shared__ int32_t roff_s[kMaxRows];
-  for (int i = threadIdx.x; i < kh + CGB_WARPS; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kh + RPS; i += blockDim.x) {
     const int64_t r = base0 + i;
     const int slot = s0 + i >= NS ? s0 + i - NS : s0 + i;
     const int sh = (sh0 + (shodd & (int)(r & 1))) & 1;
@@ -1105,35 +1110,37 @@ static __device__ __noinline__ void strip_colpass(const cgb_leaf& L, int64_t bas
   const bool two = c1 < span;
   if (c0 >= span) return;
   const int c1s = two ? c1 : c0;
-  double acc0[CGB_WARPS], xw0[CGB_WARPS], acc1[CGB_WARPS], xw1[CGB_WARPS];
+  double acc0[RPS], xw0[RPS], acc1[RPS], xw1[RPS];
 #pragma unroll
-  for (int j = 0; j < CGB_WARPS; ++j) {
+  for (int j = 0; j < RPS; ++j) {
     acc0[j] = acc1[j] = 0.0;
     xw0[j] = X(j, c0);
     xw1[j] = X(j, c1s);
   }
-  for (int g = 0; g < (kh + CGB_WARPS - 1) / CGB_WARPS; ++g) {
+  for (int g = 0; g < (kh + RPS - 1) / RPS; ++g) {
 #pragma unroll
-    for (int jj = 0; jj < CGB_WARPS; ++jj) {
-      const int a = CGB_WARPS * g + jj;
+    for (int jj = 0; jj < RPS; ++jj) {
+      const int a = RPS * g + jj;
       if (a < kh) {
         const double wa = u[conv ? kh - 1 - a : a];
 #pragma unroll
-        for (int j = 0; j < CGB_WARPS; ++j) {
-          acc0[j] = fma(wa, xw0[(jj + j) % CGB_WARPS], acc0[j]);
-          acc1[j] = fma(wa, xw1[(jj + j) % CGB_WARPS], acc1[j]);
+        for (int j = 0; j < RPS; ++j) {
+          acc0[j] = fma(wa, xw0[(jj + j) % RPS], acc0[j]);
+          acc1[j] = fma(wa, xw1[(jj + j) % RPS], acc1[j]);
         }
-        if (a + 1 < kh) {                       // slot jj: row a -> row a + 8
-          xw0[jj] = X(a + CGB_WARPS, c0);
-          xw1[jj] = X(a + CGB_WARPS, c1s);
+        if (a + 1 < kh) {                       // slot jj: row a -> row a + RPS
+          xw0[jj] = X(a + RPS, c0);
+          xw1[jj] = X(a + RPS, c1s);
         }
       }
     }
   }
+  // output row j of the step: warp j % 8's buffer j / 8
 #pragma unroll
-  for (int j = 0; j < CGB_WARPS; ++j) {
-    tbase[(size_t)j * tstride + c0] = acc0[j];
-    if (two) tbase[(size_t)j * tstride + c1] = acc1[j];
+  for (int j = 0; j < RPS; ++j) {
+    double* tj = tbase + (size_t)(j % CGB_WARPS) * tstride + (size_t)(j / CGB_WARPS) * SLOT;
+    tj[c0] = acc0[j];
+    if (two) tj[c1] = acc1[j];
   }
 }
 
@@ -1173,7 +1180,11 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
   double* ring = cgb_dyn_smem;
   // per warp: transpose buffer | two t buffers (separable strips alternate
   // them, so a step needs only the barrier after its column pass)
-  const int WSTRIDE = 2 * SLOT + 32 * CGB_RC + 2;
+  // (one t buffer per row of the warp; a second one alternating by step
+  // when a warp has one row -- not needed for correctness: the column
+  // pass's own barrier orders the writes after every row pass)
+  constexpr int TB = CGB_STRIP_RPW == 1 ? 2 : CGB_STRIP_RPW;
+  const int WSTRIDE = TB * SLOT + 32 * CGB_RC + 2;
   double* os = ring + (size_t)NS * SLOT + (size_t)wib * WSTRIDE;
   const unsigned issuer = blockDim.x - 32;  // lane 0 of the last warp (one column)
   bool any = false;
@@ -1216,14 +1227,15 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
       const int nvalid = (int)(OW - oj0 < 32 * CGB_RC ? OW - oj0 : 32 * CGB_RC);
       const int64_t clo = conv ? oj0 - (kw - 1) : oj0;
       const bool tma = clo >= 0 && clo + span <= IW;
-      const int nsteps = (int)((p1 - p0 + CGB_WARPS - 1) / CGB_WARPS);
+      constexpr int RPS = CGB_STRIP_RPS, RPW = CGB_STRIP_RPW;
+      const int nsteps = (int)((p1 - p0 + RPS - 1) / RPS);
       // input rows first needed at step s, clipped to the image and to the
       // rows this task's outputs reach
       const int64_t row_hi = oi_first + p1 - 1 + (conv ? 0 : kh - 1) + 1;
       auto batch = [&](int st, int64_t& r0, int64_t& r1) {
-        const int64_t lo = oi_first + p0 + (int64_t)CGB_WARPS * st - (conv ? kh - 1 : 0);
+        const int64_t lo = oi_first + p0 + (int64_t)RPS * st - (conv ? kh - 1 : 0);
         r0 = st == 0 ? lo : lo + kh - 1;
-        r1 = lo + kh - 1 + CGB_WARPS;
+        r1 = lo + kh - 1 + RPS;
         if (r0 < 0) r0 = 0;
         if (r1 > IH) r1 = IH;
         if (r1 > row_hi) r1 = row_hi;
@@ -1264,8 +1276,8 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
       CGB_TL(12)
       for (int st = 0; st < nsteps; ++st) {
         if (tl) tl[13] += 1.0;
-        {  // L2 prefetch of the operands this warp's NEXT output row segment reads
-          const int64_t pn = p0 + (int64_t)CGB_WARPS * (st + 1) + wib;
+        for (int k = 0; k < RPW; ++k) {  // L2 prefetch: this warp's NEXT step rows
+          const int64_t pn = p0 + (int64_t)RPS * (st + 1) + wib + CGB_WARPS * k;
           if (pn < p1) {
             const int64_t rn = rb.row_begin + pn * OW + oj0;
             epi_prefetch(epi, rn, nvalid, lane, 0);
@@ -1289,15 +1301,15 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
           __syncthreads();
         }
         CGB_TL(8)
-        const int64_t p = p0 + (int64_t)CGB_WARPS * st + wib;
-        double* tb = os + 32 * CGB_RC + 2 + (st & 1) * SLOT;
         if (sep) {
-          // all threads: column sums of the step's 8 output rows
-          const int64_t o0 = oi_first + p0 + (int64_t)CGB_WARPS * st;
+          // all threads: column sums of the step's RPS output rows
+          const int64_t o0 = oi_first + p0 + (int64_t)RPS * st;
           const int sh0 = tma ? (int)((reinterpret_cast<uintptr_t>(x + clo) >> 3) & 1) : 0;
           strip_colpass(L, conv ? o0 - (kh - 1) : o0, IH, span, ring, SLOT, NS, sh0,
                         tma ? (int)(IW & 1) : 0, taps + ntaps,
-                        ring + (size_t)NS * SLOT + 32 * CGB_RC + 2 + (st & 1) * SLOT, WSTRIDE);
+                        ring + (size_t)NS * SLOT + 32 * CGB_RC + 2 +
+                            (RPW == 1 ? (st & 1) * SLOT : 0),
+                        WSTRIDE);
           CGB_TL(9)
           __syncthreads();
           // the rows only this step read are free: batch st + 2 goes now,
@@ -1305,21 +1317,19 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
           if (tma && threadIdx.x == issuer && st + 2 < nsteps) issue(st + 2);
           CGB_TL(10)
         }
-        if (p < p1) {
-          const int64_t oi = oi_first + p;
-          int64_t a_lo = 0, a_hi = kh - 1;
-          if (conv) {
-            a_lo = oi - (IH - 1) > 0 ? oi - (IH - 1) : 0;
-            a_hi = oi < kh - 1 ? oi : kh - 1;
-          }
-          // the tile of output row p, columns [oj0, oj0 + nvalid): every term
-          // in order.  The terms before the strip term are summed first, so
-          // their global loads are in flight during the row pass; then the
-          // strip term from y, then the rest -- the same order as a tile.
-          const int64_t row0 = rb.row_begin + p * OW + oj0;
-          double acc[CGB_RC];
+        // this warp's rows of the step: p = p0 + RPS st + wib + 8 k.  The
+        // terms ahead of the strip term are summed first for every row (their
+        // loads overlap the row passes), then per row: the strip term from
+        // its row pass, the remaining terms, the epilogue -- every tile's
+        // terms in their order.
+        double accs[RPW][CGB_RC];
 #pragma unroll
-          for (int r = 0; r < CGB_RC; ++r) acc[r] = 0.0;
+        for (int k = 0; k < RPW; ++k) {
+#pragma unroll
+          for (int r = 0; r < CGB_RC; ++r) accs[k][r] = 0.0;
+          const int64_t p = p0 + (int64_t)RPS * st + wib + CGB_WARPS * k;
+          if (p >= p1) continue;
+          const int64_t row0 = rb.row_begin + p * OW + oj0;
           for (int t = rb.term_begin; t < rb.strip_term; ++t) {
             const cgb_term tt = P.terms[t];
             const cgb_leaf LL = P.leaves[tt.leaf];
@@ -1327,9 +1337,22 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
                                   ? in.shift(tt.in_off)
                                   : InVec{temp + P.temp_off[tt.in_buf - 1] + tt.in_off, nullptr,
                                           0.0};
-            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
+            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, accs[k], lane,
                          nullptr, nullptr, os, nullptr, 0);
           }
+        }
+#pragma unroll
+        for (int k = 0; k < RPW; ++k) {
+          const int64_t p = p0 + (int64_t)RPS * st + wib + CGB_WARPS * k;
+          if (p >= p1) continue;
+          double* tb = os + 32 * CGB_RC + 2 + (RPW == 1 ? (st & 1) : k) * SLOT;
+          const int64_t oi = oi_first + p;
+          int64_t a_lo = 0, a_hi = kh - 1;
+          if (conv) {
+            a_lo = oi - (IH - 1) > 0 ? oi - (IH - 1) : 0;
+            a_hi = oi < kh - 1 ? oi : kh - 1;
+          }
+          const int64_t row0 = rb.row_begin + p * OW + oj0;
           double y[CGB_RC];
           if (sep)
             strip_rowpass(kw, tb, taps, y, lane);
@@ -1339,7 +1362,7 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
           for (int t = rb.strip_term; t < rb.term_end; ++t) {
             const cgb_term tt = P.terms[t];
             if (t == rb.strip_term) {
-              tile_transpose(y, os, acc, tt.alpha, nvalid, lane);
+              tile_transpose(y, os, accs[k], tt.alpha, nvalid, lane);
               continue;
             }
             const cgb_leaf LL = P.leaves[tt.leaf];
@@ -1347,16 +1370,16 @@ __device__ bool run_strips(const DevPlan& P, int e, const InVec& in, int ts, Epi
                                   ? in.shift(tt.in_off)
                                   : InVec{temp + P.temp_off[tt.in_buf - 1] + tt.in_off, nullptr,
                                           0.0};
-            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, acc, lane,
-                             nullptr, nullptr, os, nullptr, 0);
+            leaf_tile<0>(LL, row0 - tt.row_origin, nvalid, CGB_RC, tin, tt.alpha, accs[k], lane,
+                         nullptr, nullptr, os, nullptr, 0);
           }
           if (rb.out_buf == 0) {
-            epi.tile(row0 + lane, row0, CGB_RC, nvalid - lane, acc, part);
+            epi.tile(row0 + lane, row0, CGB_RC, nvalid - lane, accs[k], part);
           } else {
             double* dst = P.temp[ts] + P.temp_off[rb.out_buf - 1] + row0 + lane;
 #pragma unroll
             for (int r = 0; r < CGB_RC; ++r)
-              if (lane + 32 * r < nvalid) dst[32 * r] = acc[r];
+              if (lane + 32 * r < nvalid) dst[32 * r] = accs[k][r];
           }
         }
         CGB_TL(11)
