@@ -745,6 +745,7 @@ struct ScsArgs {
   double* prof;    // PROF_N phase times (ns) or null
   int no_skip;     // 1: stream all of b and c (CGB_SCS_NO_ZERO_SKIP)
   double* park;    // m: large-SOC source between passes A and B (the CG scratch t), or null
+  int refresh;     // > 0: recompute A cgx, A^T A cgx every `refresh` iterations
 };
 
 // [first, last + 1) of the nonzeros of b (slots 0, 1) and c (slots 2, 3),
@@ -980,6 +981,23 @@ __global__ void __launch_bounds__(CGB_BLOCK, CGB_MINB) k_scs(const __grid_consta
     const bool need_resid = is_check || a.resid_every;
     const int write_u = need_resid || last;
 
+    // -- optional refresh of the tracked products from the warm start:
+    //    tax = A cgx, gx = A^T tax, bax = b.tax (they are otherwise carried
+    //    through the CG updates and accumulate rounding)
+    if (a.refresh > 0 && k > 0.5 && fmod(k, (double)a.refresh) < 0.5) {
+      {
+        EpiStore st1{W.tax};
+        apply_plan<TD>(F, InVec{W.cgx, nullptr, 0.0}, st1, nullptr, gs);
+      }
+      gs.sync();
+      {
+        EpiStore st2{W.gx};
+        apply_plan<TD>(Aj, InVec{W.tax, nullptr, 0.0}, st2, nullptr, gs);
+        double sb[1] = {side_dot(m, a.b, W.tax)};
+        gs.reduce(sb);
+        bax = sb[0];
+      }
+    }
     // -- subspace step: rhs = w_x - A^T w_y ; r0 = rhs - (x0 + A^T A x0)
     //    (scs.py:349-357); c.x0 and the b.w_y of the last cone step ride along
     double s[4] = {0.0, 0.0, 0.0, bwy_part};
@@ -2165,6 +2183,8 @@ int cgb_scs_run(cgb_ctx* ctx, const cgb_scs_problem* prob, const cgb_scs_setting
   a.prof = ctx->prof;
   a.no_skip = (prob->flags & CGB_SCS_NO_ZERO_SKIP) ? 1 : 0;
   a.park = std::getenv("CGB_NO_SOC_PARK") ? nullptr : work->t;
+  a.refresh = 0;
+  if (const char* env = std::getenv("CGB_REFRESH")) a.refresh = std::max(0, std::atoi(env));
   // shared memory: conv staging of the plans, or the large-SOC stash of the
   // cone step, whichever is larger (never live together; one CTA per SM --
   // the kernel re-checks the stash need with the real grid)
