@@ -583,7 +583,7 @@ def run_reference(args) -> None:
     wl = make_workload(args)
     iters = args.cpu_iters or wl.ref_iters
     orc = _OracleRun(wl)
-    for _ in range(min(args.warmup, 1)):   # the CPU has no warm-up beyond the first
+    for _ in range(args.warmup):
         orc.run(iters)
     times = [orc.run(iters) for _ in range(args.steps)]
     total = sum(times)
@@ -591,7 +591,7 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
-        "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * total / len(times),
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": _config(wl, 1, _step_iters(args, wl)),
         "setup_s": orc.setup_s,
