@@ -695,15 +695,46 @@ static __device__ __noinline__ void conv2d_tile(const cgb_leaf& L, int64_t lrow0
 // instantiation -- which calls dense_tile -- for plans with dense leaves,
 // and the others keep the inline copy (the call site cost the convolution
 // plans ~8 % when always present).
+// Row-chunk prefetch of dense_tile.  ptxas schedules each load of the
+// out-of-line callee next to its FMA (~5-8 loads in flight per lane: its
+// register budget; loading a whole chunk first did not change that), so a
+// GEMV streaming from HBM is latency-exposed.  The warp prefetches the row
+// chunks CGB_DENSE_PF chunks ahead into L1 (no registers needed: lane l
+// takes line l % 8 of rows l / 8 and l / 8 + 4 of the 8 x 1 KB chunk) and
+// the loads hit L1: configs[4] 4-7 % faster per iteration at distance 2,
+// slower at 4.  Same loads, same FMA order as dense_rows (bitwise identical
+// trajectories).
+#ifndef CGB_DENSE_PF
+#define CGB_DENSE_PF 2
+#endif
+#ifndef CGB_DENSE_PF_MIN
+#define CGB_DENSE_PF_MIN (int64_t(1) << 22)  // entries (32 MB of values)
+#endif
+__device__ __forceinline__ void dense_prefetch(const double* base, int64_t ld, int nrows,
+                                               int64_t cchunk, int64_t cols, int lane) {
+  const int64_t c = cchunk + 16 * (lane & 7);
+  if (c >= cols) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = (lane >> 3) + 4 * h;
+    if (q < nrows) asm volatile("prefetch.global.L1 [%0];" ::"l"(base + q * ld + c));
+  }
+}
+
 static __device__ __noinline__ void dense_tile(const cgb_leaf& L, int64_t lrow0, int nvalid,
                                                InVec in, double alpha, double (&acc)[CGB_RC],
                                                int lane) {
   constexpr int CGB_DR = CGB_DENSE_DR;
   constexpr int CGB_DU = CGB_DENSE_UNROLL;
+  constexpr int64_t CH = 32 * CGB_DU;  // columns per chunk
   double mine[CGB_RC];
 #pragma unroll
   for (int r = 0; r < CGB_RC; ++r) mine[r] = 0.0;
   const int64_t cols = L.cols;
+  // matrices far larger than L2 stream from HBM: prefetch; small ones are
+  // L2-resident and the prefetch only adds issue slots (configs[0]: 25 %
+  // slower with it)
+  const bool stream = L.rows * cols >= CGB_DENSE_PF_MIN;
   for (int rr0 = 0; rr0 < nvalid; rr0 += CGB_DR) {
     double sacc[CGB_DR];
     const double* rowp[CGB_DR];
@@ -713,11 +744,30 @@ static __device__ __noinline__ void dense_tile(const cgb_leaf& L, int64_t lrow0,
       const int rr = rr0 + q < nvalid ? rr0 + q : nvalid - 1;  // clamped
       rowp[q] = L.val + (lrow0 + rr) * L.ld;
     }
-#pragma unroll CGB_DU
-    for (int64_t c = lane; c < cols; c += 32) {
-      const double xv = in(c);
+    if (stream) {
+      const double* base = L.val + (lrow0 + rr0) * L.ld;
+      const int nr = nvalid - rr0 < CGB_DR ? nvalid - rr0 : CGB_DR;
 #pragma unroll
-      for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+      for (int k = 0; k < CGB_DENSE_PF; ++k) dense_prefetch(base, L.ld, nr, k * CH, cols, lane);
+      for (int64_t c0 = 0; c0 < cols; c0 += CH) {
+        dense_prefetch(base, L.ld, nr, c0 + CGB_DENSE_PF * CH, cols, lane);
+#pragma unroll
+        for (int u = 0; u < CGB_DU; ++u) {
+          const int64_t c = c0 + 32 * u + lane;
+          if (c < cols) {
+            const double xv = in(c);
+#pragma unroll
+            for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+          }
+        }
+      }
+    } else {
+#pragma unroll CGB_DU
+      for (int64_t c = lane; c < cols; c += 32) {
+        const double xv = in(c);
+#pragma unroll
+        for (int q = 0; q < CGB_DR; ++q) sacc[q] += __ldg(rowp[q] + c) * xv;
+      }
     }
 #pragma unroll
     for (int q = 0; q < CGB_DR; ++q) {
