@@ -453,12 +453,32 @@ __device__ __forceinline__ void stream_loop(int64_t n, F& f) {
 // (the ragged batch loads clamped indices).  Contiguous per-CTA ranges fed
 // by TMA bulk copies were measured slower on B200 for these 1e6-element
 // passes (one block-wide sync per chunk), see DESIGN.md.
+//
+// CGB_STREAM_PF: the warp prefetches the next batch's lines of every input
+// (lane l < 2 U takes line l & 1 of chunk u = l / 2) into L2 (1, default)
+// or L1 (2) before waiting on this batch; 0 = off.  Measured per iteration
+// (profiles/r02/ab_stream_prefetch.txt): deconv2d -1.1 %, deconv1d -1.7 %,
+// sparse lasso -2.3 %, L1 and L2 alike; trajectories bitwise unchanged.
+#ifndef CGB_STREAM_PF
+#define CGB_STREAM_PF 1
+#endif
 template <int NIN, class F>
 __device__ __forceinline__ void bulk_stream(int64_t n, const double* const (&src)[NIN], F& f) {
   const int64_t S = gsize();
   int b = 0;
   for (int64_t base = gtid(); base < n; base += CGB_U * S, ++b) {
     const bool full = base + (CGB_U - 1) * S < n;
+    if (CGB_STREAM_PF) {
+      const int lane = threadIdx.x & 31;
+      const int64_t ip = base - lane + CGB_U * S + (lane >> 1) * S + 16 * (lane & 1);
+      if (lane < 2 * CGB_U && ip < n) {
+#pragma unroll
+        for (int a = 0; a < NIN; ++a) {
+          if (CGB_STREAM_PF == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(src[a] + ip));
+          else asm volatile("prefetch.global.L1 [%0];" ::"l"(src[a] + ip));
+        }
+      }
+    }
     double v[CGB_U][NIN];
 #pragma unroll
     for (int u = 0; u < CGB_U; ++u) {
